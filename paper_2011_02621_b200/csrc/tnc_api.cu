@@ -1,0 +1,430 @@
+// libtnc C ABI: argument validation, kernel selection, launches.
+// Declarations and the reference interfaces each entry point replaces are in
+// include/tnc.h.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+#include <string>
+#include <vector>
+#include "tnc_kernels.cuh"
+#include "tnc_pair.cuh"
+#include "tnc_tc.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(TNC_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return TNC_OK;
+}
+
+int grid_for(int64_t work, int threads, int64_t cap = 148LL * 64) {
+  int64_t b = (work + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > cap) b = cap;
+  return (int)b;
+}
+
+template <typename R>
+int launch_project(const tnc_project_desc& d, cudaStream_t s) {
+  int64_t elems = 1;
+  for (int j = 0; j < d.nd; ++j) elems *= d.dim[j];
+  if (d.Z <= 0) return TNC_OK;
+  tnc::k_project<R><<<grid_for(d.Z * elems, 256), 256, 0, s>>>(d, elems);
+  return check_launch("tnc_project");
+}
+
+template <typename R, int NMAX>
+void skinny_acc(const tnc_step_desc& d, cudaStream_t s) {
+  const int64_t rows = d.Z * d.M;
+  tnc::k_step_skinny_acc<R, NMAX><<<(unsigned)((rows + 127) / 128), 128, 0, s>>>(d);
+}
+template <typename R, int KMAX>
+void skinny_row(const tnc_step_desc& d, cudaStream_t s) {
+  const int64_t rows = d.Z * d.M;
+  tnc::k_step_skinny_row<R, KMAX><<<(unsigned)((rows + 127) / 128), 128, 0, s>>>(d);
+}
+
+template <typename R>
+bool try_skinny(const tnc_step_desc& d, cudaStream_t s) {
+  if (!d.a_rows_contig || !d.b_dense || d.conj_b) return false;
+  if (d.Z * d.M > (int64_t)0x7fffffff * 128) return false;
+  const int64_t N = d.N, K = d.K;
+  if (N <= 32) {
+    if (N <= 1) skinny_acc<R, 1>(d, s);
+    else if (N <= 2) skinny_acc<R, 2>(d, s);
+    else if (N <= 4) skinny_acc<R, 4>(d, s);
+    else if (N <= 8) skinny_acc<R, 8>(d, s);
+    else if (N <= 16) skinny_acc<R, 16>(d, s);
+    else skinny_acc<R, 32>(d, s);
+    return true;
+  }
+  if (K <= 32) {
+    if (K <= 1) skinny_row<R, 1>(d, s);
+    else if (K <= 2) skinny_row<R, 2>(d, s);
+    else if (K <= 4) skinny_row<R, 4>(d, s);
+    else if (K <= 8) skinny_row<R, 8>(d, s);
+    else if (K <= 16) skinny_row<R, 16>(d, s);
+    else skinny_row<R, 32>(d, s);
+    return true;
+  }
+  return false;
+}
+
+template <typename R>
+void generic(const tnc_step_desc& d, cudaStream_t s) {
+  constexpr int BM = 64, BN = 32, BK = 16, TM = 4, TN = 2;
+  const int64_t tm = (d.M + BM - 1) / BM, tn = (d.N + BN - 1) / BN;
+  tnc::k_step_generic<R, BM, BN, BK, TM, TN><<<(unsigned)(d.Z * tm * tn), (BM / TM) * (BN / TN), 0, s>>>(d, tm, tn);
+}
+
+template <typename R>
+int launch_step(const tnc_step_desc& d, cudaStream_t s) {
+  if (d.Z <= 0 || d.M <= 0 || d.N <= 0) return TNC_OK;
+  if (d.K <= 0) return fail(TNC_E_INVALID, "tnc_step: K must be >= 1");
+  if (d.nf < 0 || d.nf > TNC_MAX_LEGS) return fail(TNC_E_INVALID, "tnc_step: nf=%d", d.nf);
+  if (d.site.ncut < 0 || d.site.ncut > TNC_MAX_CUTS) return fail(TNC_E_INVALID, "tnc_step: ncut=%d", d.site.ncut);
+  int kernel = d.kernel;
+  if (kernel == TNC_K_TC || kernel == TNC_K_AUTO) {
+    int rc = tnc::try_tc<R>(d, s);
+    if (rc == 1) return check_launch("tnc_step[tc]");
+    if (kernel == TNC_K_TC) return fail(TNC_E_UNSUPPORTED, "tnc_step: shape outside the tensor-core kernel envelope");
+  }
+  if (kernel == TNC_K_SKINNY || kernel == TNC_K_AUTO) {
+    if (try_skinny<R>(d, s)) return check_launch("tnc_step[skinny]");
+    if (kernel == TNC_K_SKINNY) return fail(TNC_E_UNSUPPORTED, "tnc_step: shape outside the skinny kernel envelope");
+  }
+  if (d.a_koff == nullptr || d.b_koff == nullptr || d.b_noff == nullptr || d.c_noff == nullptr)
+    return fail(TNC_E_INVALID, "tnc_step: generic kernel needs all four offset tables");
+  generic<R>(d, s);
+  return check_launch("tnc_step[generic]");
+}
+
+template <typename R>
+int launch_slice_sum(const tnc_slice_sum_desc& d, cudaStream_t s) {
+  if (d.B <= 0) return TNC_OK;
+  const int64_t threads = d.B * 32;
+  tnc::k_slice_sum<R><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(d);
+  return check_launch("tnc_slice_sum");
+}
+
+bool dtype_ok(int dt) { return dt == TNC_C64 || dt == TNC_C128; }
+
+template <typename R, typename KFN>
+int launch_tiled_fn(KFN kern, const tnc::PairTile& p, int64_t batch, const void* a, const void* b, void* out,
+                    cudaStream_t s) {
+  using C = typename tnc::cplx<R>::T;
+  const size_t smem = (size_t)(p.Kout * p.Lseg + p.K * p.N) * sizeof(C) + (size_t)p.K * 4;
+  if (smem > 48 * 1024) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return check_launch("tnc_contract_pair: smem attribute");
+  }
+  const int64_t blocks = batch * p.U;
+  if (blocks <= 0) return TNC_OK;
+  if (blocks > 0x7fffffffLL) return fail(TNC_E_UNSUPPORTED, "tnc_contract_pair: grid too large");
+  kern<<<(unsigned)blocks, 256, smem, s>>>(p, a, b, out);
+  return check_launch("tnc_contract_pair[tiled]");
+}
+
+template <typename R>
+int launch_pair_tiled(const tnc::PairTile& p, int64_t batch, const void* a, const void* b, void* out,
+                      cudaStream_t s) {
+  const int64_t N = p.N, K = p.K;
+  if (N <= 32) {
+    if (N <= 1) return launch_tiled_fn<R>(tnc::k_pair_tiled_acc<R, 1>, p, batch, a, b, out, s);
+    if (N <= 2) return launch_tiled_fn<R>(tnc::k_pair_tiled_acc<R, 2>, p, batch, a, b, out, s);
+    if (N <= 4) return launch_tiled_fn<R>(tnc::k_pair_tiled_acc<R, 4>, p, batch, a, b, out, s);
+    if (N <= 8) return launch_tiled_fn<R>(tnc::k_pair_tiled_acc<R, 8>, p, batch, a, b, out, s);
+    if (N <= 16) return launch_tiled_fn<R>(tnc::k_pair_tiled_acc<R, 16>, p, batch, a, b, out, s);
+    return launch_tiled_fn<R>(tnc::k_pair_tiled_acc<R, 32>, p, batch, a, b, out, s);
+  }
+  if (K <= 1) return launch_tiled_fn<R>(tnc::k_pair_tiled_row<R, 1>, p, batch, a, b, out, s);
+  if (K <= 2) return launch_tiled_fn<R>(tnc::k_pair_tiled_row<R, 2>, p, batch, a, b, out, s);
+  if (K <= 4) return launch_tiled_fn<R>(tnc::k_pair_tiled_row<R, 4>, p, batch, a, b, out, s);
+  if (K <= 8) return launch_tiled_fn<R>(tnc::k_pair_tiled_row<R, 8>, p, batch, a, b, out, s);
+  return launch_tiled_fn<R>(tnc::k_pair_tiled_row<R, 16>, p, batch, a, b, out, s);
+}
+
+}  // namespace
+
+extern "C" {
+
+int tnc_version(void) { return 100; }
+
+size_t tnc_struct_size(int which) {
+  switch (which) {
+    case 0: return sizeof(tnc_site);
+    case 1: return sizeof(tnc_step_desc);
+    case 2: return sizeof(tnc_project_desc);
+    case 3: return sizeof(tnc_slice_sum_desc);
+    case 4: return sizeof(tnc_path_desc);
+    default: return 0;
+  }
+}
+
+const char* tnc_last_error(void) { return g_err.c_str(); }
+
+int tnc_device_check(void) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(TNC_E_NODEVICE, "no CUDA device");
+  cudaDeviceProp p;
+  if (cudaGetDeviceProperties(&p, dev) != cudaSuccess) return fail(TNC_E_NODEVICE, "cudaGetDeviceProperties failed");
+  if (p.major != 10) return fail(TNC_E_NODEVICE, "device %s is sm_%d%d, libtnc is built for sm_100a", p.name, p.major, p.minor);
+  return TNC_OK;
+}
+
+int tnc_project(const tnc_project_desc* d, void* stream) {
+  if (!d || !dtype_ok(d->dtype)) return fail(TNC_E_INVALID, "tnc_project: bad descriptor");
+  if (d->nd < 0 || d->nd > TNC_MAX_LEGS) return fail(TNC_E_INVALID, "tnc_project: nd=%d", d->nd);
+  if (d->slices_per_b <= 0) return fail(TNC_E_INVALID, "tnc_project: slices_per_b must be >= 1");
+  cudaStream_t s = (cudaStream_t)stream;
+  return d->dtype == TNC_C64 ? launch_project<float>(*d, s) : launch_project<double>(*d, s);
+}
+
+int tnc_step(const tnc_step_desc* d, void* stream) {
+  if (!d || !dtype_ok(d->dtype)) return fail(TNC_E_INVALID, "tnc_step: bad descriptor");
+  if (d->slices_per_b <= 0) return fail(TNC_E_INVALID, "tnc_step: slices_per_b must be >= 1");
+  cudaStream_t s = (cudaStream_t)stream;
+  return d->dtype == TNC_C64 ? launch_step<float>(*d, s) : launch_step<double>(*d, s);
+}
+
+int tnc_slice_sum(const tnc_slice_sum_desc* d, void* stream) {
+  if (!d || !dtype_ok(d->dtype) || d->slices_per_b <= 0) return fail(TNC_E_INVALID, "tnc_slice_sum: bad descriptor");
+  cudaStream_t s = (cudaStream_t)stream;
+  return d->dtype == TNC_C64 ? launch_slice_sum<float>(*d, s) : launch_slice_sum<double>(*d, s);
+}
+
+int tnc_contract_path(const tnc_path_desc* d, void* stream) {
+  if (!d || d->nsteps < 0 || (d->nsteps > 0 && !d->steps)) return fail(TNC_E_INVALID, "tnc_contract_path: bad descriptor");
+  int rc = tnc_project(&d->first, stream);
+  if (rc) return rc;
+  for (int i = 0; i < d->nsteps; ++i) {
+    rc = tnc_step(&d->steps[i], stream);
+    if (rc) {
+      std::string m = g_err;
+      return fail(rc, "step %d: %s", i, m.c_str());
+    }
+  }
+  return tnc_slice_sum(&d->reduce, stream);
+}
+
+// ---------------------------------------------------------------------------
+// contract_pair: builds a one-step descriptor on the host, stages its offset
+// tables into the caller's device workspace and runs tnc_step.
+// ---------------------------------------------------------------------------
+static void pair_layout(int a_rank, const int64_t* a_dims, int b_rank, const int64_t* b_dims,
+                        int npairs, const int32_t* pa, const int32_t* pb,
+                        std::vector<int>& fa, std::vector<int>& fb, int64_t& K, int64_t& N) {
+  std::vector<char> ua(a_rank, 0), ub(b_rank, 0);
+  for (int i = 0; i < npairs; ++i) { ua[pa[i]] = 1; ub[pb[i]] = 1; }
+  fa.clear(); fb.clear();
+  for (int i = 0; i < a_rank; ++i) if (!ua[i]) fa.push_back(i);
+  for (int i = 0; i < b_rank; ++i) if (!ub[i]) fb.push_back(i);
+  K = 1; N = 1;
+  for (int i = 0; i < npairs; ++i) K *= a_dims[pa[i]];
+  for (int i : fb) N *= b_dims[i];
+}
+
+size_t tnc_contract_pair_workspace(int a_rank, const int64_t* a_dims, int b_rank, const int64_t* b_dims,
+                                   int npairs, const int32_t* pair_a, const int32_t* pair_b) {
+  std::vector<int> fa, fb;
+  int64_t K, N;
+  pair_layout(a_rank, a_dims, b_rank, b_dims, npairs, pair_a, pair_b, fa, fb, K, N);
+  // generic tables + tiled-kernel tables (segoff <= K int64, rowoff <= 8192 int32, koff K int32)
+  return (size_t)(2 * K + 2 * N) * sizeof(int64_t) + (size_t)K * 8 + 8192 * 4 + (size_t)K * 4 + 256;
+}
+
+int tnc_contract_pair(int dtype, int64_t batch,
+                      const void* a, int a_rank, const int64_t* a_dims, int64_t a_zstride,
+                      const void* b, int b_rank, const int64_t* b_dims, int64_t b_zstride,
+                      int npairs, const int32_t* pair_a, const int32_t* pair_b,
+                      const int32_t* out_perm, int conj_b,
+                      void* out, int64_t out_zstride,
+                      void* workspace, size_t workspace_bytes, void* stream) {
+  if (!dtype_ok(dtype)) return fail(TNC_E_INVALID, "tnc_contract_pair: bad dtype %d", dtype);
+  if (a_rank < 0 || b_rank < 0 || a_rank > TNC_MAX_LEGS || b_rank > TNC_MAX_LEGS)
+    return fail(TNC_E_INVALID, "tnc_contract_pair: rank out of range");
+  std::vector<char> ua(a_rank, 0), ub(b_rank, 0);
+  for (int i = 0; i < npairs; ++i) {
+    if (pair_a[i] < 0 || pair_a[i] >= a_rank || pair_b[i] < 0 || pair_b[i] >= b_rank)
+      return fail(TNC_E_INVALID, "axis pair (%d, %d) out of range", pair_a[i], pair_b[i]);
+    if (ua[pair_a[i]] || ub[pair_b[i]]) return fail(TNC_E_INVALID, "axis repeated in pairs: (%d, %d)", pair_a[i], pair_b[i]);
+    ua[pair_a[i]] = ub[pair_b[i]] = 1;
+    if (a_dims[pair_a[i]] != b_dims[pair_b[i]])
+      return fail(TNC_E_INVALID, "extent mismatch on pair (%d, %d)", pair_a[i], pair_b[i]);
+  }
+  std::vector<int> fa, fb;
+  int64_t K, N;
+  pair_layout(a_rank, a_dims, b_rank, b_dims, npairs, pair_a, pair_b, fa, fb, K, N);
+  if (workspace_bytes < (size_t)(2 * K + 2 * N) * sizeof(int64_t))
+    return fail(TNC_E_INVALID, "tnc_contract_pair: workspace too small");
+  // row-major strides of a and b
+  std::vector<int64_t> sa(a_rank), sb(b_rank);
+  { int64_t s = 1; for (int i = a_rank - 1; i >= 0; --i) { sa[i] = s; s *= a_dims[i]; } }
+  { int64_t s = 1; for (int i = b_rank - 1; i >= 0; --i) { sb[i] = s; s *= b_dims[i]; } }
+  // output axes: free a then free b, permuted by out_perm
+  const int nout = (int)(fa.size() + fb.size());
+  std::vector<int64_t> odims(nout);
+  for (size_t i = 0; i < fa.size(); ++i) odims[i] = a_dims[fa[i]];
+  for (size_t i = 0; i < fb.size(); ++i) odims[fa.size() + i] = b_dims[fb[i]];
+  std::vector<int> perm(nout);
+  for (int i = 0; i < nout; ++i) perm[i] = out_perm ? out_perm[i] : i;
+  std::vector<char> seen(nout, 0);
+  for (int i = 0; i < nout; ++i) {
+    if (perm[i] < 0 || perm[i] >= nout || seen[perm[i]]) return fail(TNC_E_INVALID, "tnc_contract_pair: bad out_perm");
+    seen[perm[i]] = 1;
+  }
+  std::vector<int64_t> ostride_by_src(nout);  // stride in out of natural axis j
+  { int64_t s = 1; for (int i = nout - 1; i >= 0; --i) { ostride_by_src[perm[i]] = s; s *= odims[perm[i]]; } }
+
+  tnc_step_desc d;
+  memset(&d, 0, sizeof d);
+  d.dtype = dtype;
+  d.kernel = TNC_K_GENERIC;
+  d.Z = batch;
+  d.slices_per_b = 1;
+  d.acc = a; d.acc_zstride = a_zstride;
+  d.out = out; d.out_zstride = out_zstride;
+  d.site.ptr = b; d.site.zstride = b_zstride;
+  d.conj_b = conj_b ? 1 : 0;
+  d.nf = (int)fa.size();
+  d.M = 1;
+  for (size_t i = 0; i < fa.size(); ++i) {
+    d.f_dim[i] = a_dims[fa[i]];
+    d.f_astride[i] = sa[fa[i]];
+    d.f_cstride[i] = ostride_by_src[i];
+    d.M *= a_dims[fa[i]];
+  }
+  d.K = K; d.N = N;
+  std::vector<int64_t> tab(2 * K + 2 * N);
+  for (int64_t k = 0; k < K; ++k) {
+    int64_t r = k, oa = 0, ob = 0;
+    for (int i = npairs - 1; i >= 0; --i) {
+      const int64_t dm = a_dims[pair_a[i]];
+      oa += (r % dm) * sa[pair_a[i]];
+      ob += (r % dm) * sb[pair_b[i]];
+      r /= dm;
+    }
+    tab[k] = oa; tab[K + k] = ob;
+  }
+  for (int64_t n = 0; n < N; ++n) {
+    int64_t r = n, obn = 0, ocn = 0;
+    for (int i = (int)fb.size() - 1; i >= 0; --i) {
+      const int64_t dm = b_dims[fb[i]];
+      obn += (r % dm) * sb[fb[i]];
+      ocn += (r % dm) * ostride_by_src[fa.size() + i];
+      r /= dm;
+    }
+    tab[2 * K + n] = obn; tab[2 * K + N + n] = ocn;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  bool identity_a = true;  // free a legs keep their order at the front of out
+  for (size_t i = 0; i < fa.size(); ++i) identity_a = identity_a && perm[i] == (int)i;
+  const int64_t tile_max = dtype == TNC_C64 ? 8192 : 4096;
+  const bool tiled_ok = identity_a && K * N <= 4096 && (N <= 32 || K <= 16) && a_rank > 0;
+  if (tiled_ok) {
+    std::vector<char> shared(a_rank, 0);
+    for (int i = 0; i < npairs; ++i) shared[pair_a[i]] = 1;
+    // grow the segment from the innermost leg while the tile fits
+    int t = a_rank;
+    int64_t lseg = 1, kout = K;
+    while (t > 0) {
+      const int64_t d = a_dims[t - 1];
+      const int64_t nl = lseg * d, nk = shared[t - 1] ? kout / d : kout;
+      if (nk * nl > tile_max) break;
+      lseg = nl; kout = nk; --t;
+    }
+    const int64_t tile = kout * lseg;
+    const int64_t R = tile / K;
+    if (tile <= tile_max && R >= 1) {
+      tnc::PairTile pt;
+      memset(&pt, 0, sizeof pt);
+      // outer free legs / outer shared legs / inner free legs
+      std::vector<int> of, os, inf;
+      for (int i = 0; i < a_rank; ++i) {
+        if (i < t) (shared[i] ? os : of).push_back(i);
+        else if (!shared[i]) inf.push_back(i);
+      }
+      pt.nfo = (int)of.size();
+      pt.U = 1;
+      for (size_t j = 0; j < of.size(); ++j) { pt.fo_dim[j] = a_dims[of[j]]; pt.fo_stride[j] = sa[of[j]]; pt.U *= a_dims[of[j]]; }
+      pt.a_zstride = a_zstride; pt.b_zstride = b_zstride; pt.out_zstride = out_zstride;
+      pt.conj_b = conj_b ? 1 : 0;
+      pt.Kout = kout; pt.Lseg = lseg; pt.R = R; pt.K = K; pt.N = N;
+      std::vector<int64_t> segoff(kout);
+      std::vector<int64_t> segw(a_rank, 0);  // mixed-radix weight of an outer shared leg
+      { int64_t w = 1; for (int j = (int)os.size() - 1; j >= 0; --j) { segw[os[j]] = w; w *= a_dims[os[j]]; } }
+      for (int64_t j = 0; j < kout; ++j) {
+        int64_t r = j, off = 0;
+        for (int q = (int)os.size() - 1; q >= 0; --q) { off += (r % a_dims[os[q]]) * sa[os[q]]; r /= a_dims[os[q]]; }
+        segoff[j] = off;
+      }
+      std::vector<int32_t> rowoff(R), koff(K);
+      for (int64_t r0 = 0; r0 < R; ++r0) {
+        int64_t r = r0, off = 0;
+        for (int q = (int)inf.size() - 1; q >= 0; --q) { off += (r % a_dims[inf[q]]) * sa[inf[q]]; r /= a_dims[inf[q]]; }
+        rowoff[r0] = (int32_t)off;
+      }
+      for (int64_t k0 = 0; k0 < K; ++k0) {
+        int64_t r = k0, seg = 0, inner = 0;
+        for (int i = npairs - 1; i >= 0; --i) {
+          const int ax = pair_a[i];
+          const int64_t dm = a_dims[ax], dg = r % dm;
+          r /= dm;
+          if (ax < t) seg += dg * segw[ax]; else inner += dg * sa[ax];
+        }
+        koff[k0] = (int32_t)(seg * lseg + inner);
+      }
+      bool v16 = dtype == TNC_C64 && (lseg % 2 == 0) && (a_zstride % 2 == 0) && (((uintptr_t)a) % 16 == 0);
+      for (int64_t j = 0; j < kout && v16; ++j) v16 = (segoff[j] % 2 == 0);
+      pt.vec16 = v16 ? 1 : 0;
+      // workspace: [b_koff K][b_noff N] int64, segoff int64, rowoff int32, koff int32
+      unsigned char* w = reinterpret_cast<unsigned char*>(workspace);
+      size_t o_bk = 0, o_bn = o_bk + K * 8, o_seg = o_bn + N * 8, o_row = o_seg + kout * 8, o_k = o_row + R * 4;
+      const size_t total = o_k + K * 4;
+      if (total > workspace_bytes) return fail(TNC_E_INVALID, "tnc_contract_pair: workspace too small");
+      std::vector<unsigned char> blob(total);
+      memcpy(blob.data() + o_bk, tab.data() + K, K * 8);
+      memcpy(blob.data() + o_bn, tab.data() + 2 * K, N * 8);
+      memcpy(blob.data() + o_seg, segoff.data(), kout * 8);
+      memcpy(blob.data() + o_row, rowoff.data(), R * 4);
+      memcpy(blob.data() + o_k, koff.data(), K * 4);
+      if (cudaMemcpyAsync(workspace, blob.data(), total, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return check_launch("tnc_contract_pair: table upload");
+      pt.b_koff = reinterpret_cast<const int64_t*>(w + o_bk);
+      pt.b_noff = reinterpret_cast<const int64_t*>(w + o_bn);
+      pt.segoff = reinterpret_cast<const int64_t*>(w + o_seg);
+      pt.rowoff = reinterpret_cast<const int32_t*>(w + o_row);
+      pt.koff = reinterpret_cast<const int32_t*>(w + o_k);
+      int rc = dtype == TNC_C64 ? launch_pair_tiled<float>(pt, batch, a, b, out, s)
+                                : launch_pair_tiled<double>(pt, batch, a, b, out, s);
+      if (rc) return rc;
+      if (cudaStreamSynchronize(s) != cudaSuccess) return check_launch("tnc_contract_pair: sync");
+      return TNC_OK;
+    }
+  }
+  if (cudaMemcpyAsync(workspace, tab.data(), tab.size() * sizeof(int64_t), cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return check_launch("tnc_contract_pair: table upload");
+  int64_t* w = reinterpret_cast<int64_t*>(workspace);
+  d.a_koff = w; d.b_koff = w + K; d.b_noff = w + 2 * K; d.c_noff = w + 2 * K + N;
+  int rc = tnc_step(&d, stream);
+  if (rc) return rc;
+  // tab must stay alive until the async copy has consumed it
+  if (cudaStreamSynchronize(s) != cudaSuccess) return check_launch("tnc_contract_pair: sync");
+  return TNC_OK;
+}
+
+}  // extern "C"

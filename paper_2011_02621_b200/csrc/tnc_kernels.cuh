@@ -1,0 +1,255 @@
+// SIMT kernels of libtnc: projection gather, generic tiled contraction,
+// bandwidth ("skinny") contraction, slice sum.
+#pragma once
+#include "tnc_common.cuh"
+
+namespace tnc {
+
+// ---------------------------------------------------------------------------
+// Projection / slicing gather (network.py:321-335 with product-state bras,
+// network.py:446-453 cut restriction): out[z][i] = site(z)[off(i)].
+// ---------------------------------------------------------------------------
+template <typename R>
+__global__ void __launch_bounds__(256)
+k_project(const __grid_constant__ tnc_project_desc d, int64_t elems) {
+  using C = typename cplx<R>::T;
+  const C* src = reinterpret_cast<const C*>(d.site.ptr);
+  C* out = reinterpret_cast<C*>(d.out);
+  const int64_t total = d.Z * elems;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t z = g / elems;
+    int64_t i = g - z * elems;
+    int64_t off = site_offset(d.site, z, d.slices_per_b, d.s0);
+    for (int j = d.nd - 1; j >= 0; --j) {
+      const int64_t q = i / d.dim[j];
+      off += (i - q * d.dim[j]) * d.src_stride[j];
+      i = q;
+    }
+    C v = src[off];
+    if (d.conj) v = cconj(v);
+    out[z * d.out_zstride + (g - z * elems)] = v;
+  }
+}
+
+// mixed-radix row decomposition -> (acc offset, out offset)
+__device__ __forceinline__ void row_offsets(const tnc_step_desc& d, int64_t f, int64_t& oa, int64_t& oc) {
+  oa = 0; oc = 0;
+  for (int j = d.nf - 1; j >= 0; --j) {
+    const int64_t q = f / d.f_dim[j];
+    const int64_t r = f - q * d.f_dim[j];
+    oa += r * d.f_astride[j];
+    oc += r * d.f_cstride[j];
+    f = q;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Generic tiled contraction: any leg layout, any K and N.  Register-blocked
+// SIMT complex GEMM whose operand/result addresses come from the step's
+// stride tables (correctness reference kernel and catch-all).
+// ---------------------------------------------------------------------------
+template <typename R, int BM, int BN, int BK, int TM, int TN>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN))
+k_step_generic(const __grid_constant__ tnc_step_desc d, int64_t tiles_m, int64_t tiles_n) {
+  using C = typename cplx<R>::T;
+  constexpr int TX = BN / TN, TY = BM / TM, NT = TX * TY;
+  __shared__ C As[BK][BM + 1];
+  __shared__ C Bs[BK][BN + 1];
+  __shared__ int64_t rowA[BM], rowC[BM];
+
+  int64_t t = blockIdx.x;
+  const int64_t tiles = tiles_m * tiles_n;
+  const int64_t z = t / tiles;
+  t -= z * tiles;
+  const int64_t m0 = (t / tiles_n) * BM, n0 = (t % tiles_n) * BN;
+  const C* A = reinterpret_cast<const C*>(d.acc) + z * d.acc_zstride;
+  const C* B = reinterpret_cast<const C*>(d.site.ptr) + site_offset(d.site, z, d.slices_per_b, d.s0);
+  C* Co = reinterpret_cast<C*>(d.out) + z * d.out_zstride;
+
+  for (int i = threadIdx.x; i < BM; i += NT) {
+    int64_t oa = 0, oc = 0;
+    if (m0 + i < d.M) row_offsets(d, m0 + i, oa, oc);
+    rowA[i] = oa;
+    rowC[i] = oc;
+  }
+  const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
+  C acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = czero<R>();
+  __syncthreads();
+
+  for (int64_t k0 = 0; k0 < d.K; k0 += BK) {
+    for (int e = threadIdx.x; e < BM * BK; e += NT) {
+      const int i = e / BK, kk = e % BK;
+      const int64_t k = k0 + kk;
+      C v = czero<R>();
+      if (m0 + i < d.M && k < d.K) v = A[rowA[i] + d.a_koff[k]];
+      As[kk][i] = v;
+    }
+    for (int e = threadIdx.x; e < BK * BN; e += NT) {
+      const int kk = e / BN, j = e % BN;
+      const int64_t k = k0 + kk, n = n0 + j;
+      C v = czero<R>();
+      if (k < d.K && n < d.N) {
+        v = B[d.b_koff[k] + d.b_noff[n]];
+        if (d.conj_b) v = cconj(v);
+      }
+      Bs[kk][j] = v;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int kk = 0; kk < BK; ++kk) {
+      C a[TM], b[TN];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) a[i] = As[kk][ty * TM + i];
+#pragma unroll
+      for (int j = 0; j < TN; ++j) b[j] = Bs[kk][tx + j * TX];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) cfma(acc[i][j], a[i], b[j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int r = ty * TM + i;
+    if (m0 + r >= d.M) continue;
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int64_t n = n0 + tx + j * TX;
+      if (n < d.N) Co[rowC[r] + d.c_noff[n]] = acc[i][j];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Skinny contraction, accumulator-resident (N <= NMAX <= 32): one thread per
+// row of the row-contiguous accumulator; the row is streamed through
+// registers in chunks, the dense [K][N] site block is read as warp-uniform
+// broadcasts, the N results stay in registers.  HBM-bound for K*N <~ 256.
+// ---------------------------------------------------------------------------
+template <typename R, int NMAX>
+__global__ void __launch_bounds__(128)
+k_step_skinny_acc(const __grid_constant__ tnc_step_desc d) {
+  using C = typename cplx<R>::T;
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= d.Z * d.M) return;
+  const int64_t z = g / d.M, f = g - z * d.M;
+  const int K = (int)d.K, N = (int)d.N;
+  const C* __restrict__ a = reinterpret_cast<const C*>(d.acc) + z * d.acc_zstride + f * d.K;
+  const C* __restrict__ S = reinterpret_cast<const C*>(d.site.ptr) + site_offset(d.site, z, d.slices_per_b, d.s0);
+  C acc[NMAX];
+#pragma unroll
+  for (int n = 0; n < NMAX; ++n) acc[n] = czero<R>();
+  constexpr int KC = 8;
+  int k0 = 0;
+  for (; k0 + KC <= K; k0 += KC) {
+    C av[KC];
+#pragma unroll
+    for (int kk = 0; kk < KC; ++kk) av[kk] = __ldg(a + k0 + kk);
+#pragma unroll
+    for (int kk = 0; kk < KC; ++kk) {
+      const C* srow = S + (int64_t)(k0 + kk) * N;
+#pragma unroll
+      for (int n = 0; n < NMAX; ++n)
+        if (n < N) cfma(acc[n], av[kk], __ldg(srow + n));
+    }
+  }
+  for (; k0 < K; ++k0) {
+    const C av = __ldg(a + k0);
+    const C* srow = S + (int64_t)k0 * N;
+#pragma unroll
+    for (int n = 0; n < NMAX; ++n)
+      if (n < N) cfma(acc[n], av, __ldg(srow + n));
+  }
+  C* o = reinterpret_cast<C*>(d.out) + z * d.out_zstride;
+  if (d.c_rows_contig) {
+    o += f * d.N;
+#pragma unroll
+    for (int n = 0; n < NMAX; ++n)
+      if (n < N) o[n] = acc[n];
+  } else {
+    int64_t oa, oc;
+    row_offsets(d, f, oa, oc);
+#pragma unroll
+    for (int n = 0; n < NMAX; ++n)
+      if (n < N) o[oc + d.c_noff[n]] = acc[n];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Skinny contraction, row-resident (K <= KMAX <= 32, any N): the thread keeps
+// its whole accumulator row in registers and emits the N outputs in chunks.
+// ---------------------------------------------------------------------------
+template <typename R, int KMAX>
+__global__ void __launch_bounds__(128)
+k_step_skinny_row(const __grid_constant__ tnc_step_desc d) {
+  using C = typename cplx<R>::T;
+  const int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (g >= d.Z * d.M) return;
+  const int64_t z = g / d.M, f = g - z * d.M;
+  const int K = (int)d.K, N = (int)d.N;
+  const C* __restrict__ a = reinterpret_cast<const C*>(d.acc) + z * d.acc_zstride + f * d.K;
+  const C* __restrict__ S = reinterpret_cast<const C*>(d.site.ptr) + site_offset(d.site, z, d.slices_per_b, d.s0);
+  C av[KMAX];
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) av[k] = (k < K) ? __ldg(a + k) : czero<R>();
+  C* o = reinterpret_cast<C*>(d.out) + z * d.out_zstride;
+  int64_t oc = f * d.N;
+  if (!d.c_rows_contig) {
+    int64_t oa;
+    row_offsets(d, f, oa, oc);
+  }
+  constexpr int NC = 8;
+  for (int n0 = 0; n0 < N; n0 += NC) {
+    C acc[NC];
+#pragma unroll
+    for (int j = 0; j < NC; ++j) acc[j] = czero<R>();
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+      if (k < K) {
+        const C* srow = S + (int64_t)k * N + n0;
+#pragma unroll
+        for (int j = 0; j < NC; ++j)
+          if (n0 + j < N) cfma(acc[j], av[k], __ldg(srow + j));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      const int n = n0 + j;
+      if (n < N) o[d.c_rows_contig ? oc + n : oc + d.c_noff[n]] = acc[j];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Slice sum (network.py:546-551): one warp per bitstring, fixed summation
+// order (lane-strided partial sums + xor-shuffle tree) -> deterministic.
+// ---------------------------------------------------------------------------
+template <typename R>
+__global__ void __launch_bounds__(256)
+k_slice_sum(const __grid_constant__ tnc_slice_sum_desc d) {
+  using C = typename cplx<R>::T;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= d.B) return;
+  const C* x = reinterpret_cast<const C*>(d.x);
+  C s = czero<R>();
+  for (int64_t j = lane; j < d.slices_per_b; j += 32) s = cadd(s, x[(warp * d.slices_per_b + j) * d.x_zstride]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
+    s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
+  }
+  if (lane == 0) {
+    C* amp = reinterpret_cast<C*>(d.amp);
+    amp[warp] = d.accumulate ? cadd(amp[warp], s) : s;
+  }
+}
+
+}  // namespace tnc
+
