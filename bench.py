@@ -1,0 +1,479 @@
+#!/usr/bin/env python
+"""Benchmark of the contraction hot path (one JSON line on rank 0).
+
+Workloads (``--workload``):
+
+* ``sweep`` (default; BASELINE.json configs[1]) -- isolated pairwise
+  contraction sweep in complex64: the accumulator C has r free legs of dim 2
+  (r = 16..28) and k shared legs of dim 4 (k = 1..3) in a seeded random leg
+  order; it is contracted with the bitstring-projected site tensor (k shared +
+  n = 1..3 new dim-4 legs) over a bitstring batch B in {1, 16, 256}; cases are
+  kept while every operand fits 2^29 elements.  One *step* = one pass over
+  all cases; each case = projection gather + fused permute/contract kernel.
+  Unit: bitstring-steps/s (one bitstring's accumulator advanced by one
+  Contract step).  The 53-qubit / 12-cycle headline network is not runnable by
+  this algorithm on any GPU count (peak intermediate 2^41 elements unsliced,
+  see DESIGN.md), so the tier rule's "largest single-GPU configuration"
+  applies.
+* ``cfg0`` (configs[0]) -- full amplitudes: 3x3 lattice, 8 cycles, 64
+  bitstrings, complex128, projected engine.  Unit: amplitudes/s.
+
+Timing: W warm-up steps, then K steps; every case (a timed iteration) is
+bracketed by CUDA events on the launching stream and preceded by an untimed
+L2 flush (256 MiB memset), so no case reads L2-resident data; barrier +
+synchronize around the timed region; max over ranks.  ``--impl reference``
+times the CPU oracle port of the reference algorithm (numpy tensordot, as
+tnsim.tensor.contract_pair) on a bounded sample and scales to the same unit.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from math import prod
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "amplitudes/sec (53q, depth 12) at 1/2/4/8 GPUs; contraction % of roofline"
+SWEEP_LIMIT = 1 << 29          # elements per operand (complex64: 4 GiB)
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+def sweep_cases(limit=SWEEP_LIMIT):
+    cases = []
+    for r in (16, 20, 24, 28):
+        for k in (1, 2, 3):
+            for n in (1, 2, 3):
+                for B in (1, 16, 256):
+                    if B * (2 ** r) * (4 ** max(k, n)) <= limit:
+                        cases.append((r, k, n, B))
+    return cases
+
+
+def case_layout(r, k, n, seed):
+    rng = np.random.default_rng(seed)
+    perm = [int(x) for x in rng.permutation(r + k)]
+    dims = [2 if x < r else 4 for x in perm]
+    shared_pos = sorted((i for i, x in enumerate(perm) if x >= r), key=lambda i: perm[i])
+    pairs = [(p, j) for j, p in enumerate(shared_pos)]
+    return perm, dims, pairs
+
+
+def case_traffic(r, k, n, B, itemsize=8):
+    acc = B * 2 ** r * 4 ** k
+    out = B * 2 ** r * 4 ** n
+    site = B * 4 ** (k + n)
+    return (acc + out + 2 * site) * itemsize, 8 * B * 2 ** r * 4 ** k * 4 ** n
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5.0 and self.proc.poll() is None:
+                time.sleep(0.02)
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        loaded = [x for x in sm if x > 0.5 * mx] if mx else sm
+        med = float(np.median(loaded)) if loaded else None
+        out = {"sm_mhz": med, "sm_max_mhz": mx or None, "reasons": sorted(reasons), "samples": len(sm)}
+        if not sm and self.lines:
+            out["raw"] = self.lines[:2]
+        return out
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_sweep(args, rank, world, dev):
+    import torch
+
+    from paper_2011_02621_b200.engine import PairPlan, project_variants
+
+    hbm, bf16, peak_src = peaks()
+    cases = sweep_cases(args.limit)
+    torch.manual_seed(1234 + rank)
+    max_acc = max(B * 2 ** r * 4 ** k for r, k, n, B in cases)
+    max_out = max(B * 2 ** r * 4 ** n for r, k, n, B in cases)
+    acc = torch.randn(max_acc, dtype=torch.complex64, device=dev)
+    out = torch.empty(max_out, dtype=torch.complex64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    plans, inputs = [], []
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(99 + rank)
+    for ci, (r, k, n, B) in enumerate(cases):
+        perm, dims, pairs = case_layout(r, k, n, seed=ci)
+        plan = PairPlan(dims, [4] * (k + n), pairs, dtype="complex64")
+        variants = torch.randn((2, 4 ** (k + n)), dtype=torch.complex64, device=dev, generator=gen)
+        bits = torch.randint(0, 2, (B,), dtype=torch.int32, device=dev, generator=gen)
+        site = torch.empty((B, 4 ** (k + n)), dtype=torch.complex64, device=dev)
+        plans.append(plan)
+        inputs.append((variants, bits, site))
+    stream = torch.cuda.current_stream(dev)
+
+    def one_step(record):
+        tot_case, tot_kern = 0.0, 0.0
+        per = []
+        for ci, (r, k, n, B) in enumerate(cases):
+            variants, bits, site = inputs[ci]
+            KN = 4 ** (k + n)
+            flush.zero_()
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record(stream)
+            project_variants(variants, bits, site, KN, stream)
+            e1.record(stream)
+            plans[ci](acc, site, out, B, 2 ** r * 4 ** k, KN, 2 ** r * 4 ** n, stream)
+            e2.record(stream)
+            per.append((e0, e1, e2))
+        torch.cuda.synchronize(dev)
+        rows = []
+        for (r, k, n, B), (e0, e1, e2) in zip(cases, per):
+            tc = e0.elapsed_time(e2) * 1e-3
+            tk = e1.elapsed_time(e2) * 1e-3
+            tot_case += tc
+            tot_kern += tk
+            rows.append((r, k, n, B, tc, tk))
+        return tot_case, tot_kern, rows
+
+    for _ in range(args.warmup):
+        one_step(False)
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    with ClockSampler(dev.index) as clk:
+        t_case = t_kern = 0.0
+        acc_rows = {}
+        for _ in range(args.steps):
+            tc, tk, rows = one_step(True)
+            t_case += tc
+            t_kern += tk
+            for r, k, n, B, a, b in rows:
+                acc_rows.setdefault((r, k, n, B), [0.0, 0.0])
+                acc_rows[(r, k, n, B)][0] += a
+                acc_rows[(r, k, n, B)][1] += b
+    torch.cuda.synchronize(dev)
+    barrier(world)
+    t_case_max = allreduce_max(t_case, world, dev)
+    units_per_step = sum(B for _, _, _, B in cases)
+    value = world * units_per_step * args.steps / t_case_max
+    # roofline of the dominant kernel (the fused permute+contract launch)
+    bytes_tot = sum(case_traffic(*c)[0] for c in cases) * args.steps
+    flops_tot = sum(case_traffic(*c)[1] for c in cases) * args.steps
+    roof_t = sum(max(case_traffic(*c)[0] / (hbm * 1e9), case_traffic(*c)[1] / (bf16 * 1e12)) for c in cases) * args.steps
+    achieved = bytes_tot / t_kern / 1e9
+    detail = []
+    for c, (a, b) in acc_rows.items():
+        by, fl = case_traffic(*c)
+        detail.append({"r": c[0], "k": c[1], "n": c[2], "B": c[3], "kernel_us": 1e6 * b / args.steps,
+                       "GBps": by / (b / args.steps) / 1e9, "TFLOPs": fl / (b / args.steps) / 1e12})
+    res = {
+        "value": value, "unit": "bitstring-steps/s", "ms_per_step": 1e3 * t_case_max / args.steps,
+        "gpu_launches": 2 * len(cases) * args.steps,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": (roof_t / t_kern), "traffic": None,
+                     "peak_source": f"{peak_src} hbm_gbs / bf16_tflops (MEASURED_PEAKS.json)",
+                     "kernel": "tnc::k_pair_tiled_* (fused permute+contract)",
+                     "algorithmic": "per case (acc + out + 2*projected site) * 8 B; flops 8*B*2^r*4^k*4^n",
+                     "kernel_share_of_step": t_kern / t_case, "tflops_achieved": flops_tot / t_kern / 1e12},
+        "config": {"workload": "configs[1] pairwise-contraction sweep", "dtype": "complex64",
+                   "cases": len(cases), "r": [16, 20, 24, 28], "k": [1, 2, 3], "n": [1, 2, 3],
+                   "batch": [1, 16, 256], "operand_limit_elems": args.limit,
+                   "leg_order": "seeded random permutation per case",
+                   "l2": "256 MiB memset flush before every case (untimed)"},
+        "clocks": clk.summary(),
+        "dtype": "complex64",
+        "detail": detail,
+    }
+    if args.e2e:
+        res["e2e"] = sweep_e2e(args, cases, plans, inputs, dev, world)
+    return res
+
+
+def sweep_e2e(args, cases, plans, inputs, dev, world):
+    """Same sweep through the public API with host buffers: per case the
+    accumulator and projection bits go H2D from pinned memory, gather +
+    contract run, the result comes back D2H; all inside the timed region."""
+    import torch
+
+    from paper_2011_02621_b200.engine import project_variants
+
+    max_acc = max(B * 2 ** r * 4 ** k for r, k, n, B in cases)
+    max_out = max(B * 2 ** r * 4 ** n for r, k, n, B in cases)
+    h_acc = torch.randn(max_acc, dtype=torch.complex64).pin_memory()
+    h_out = torch.empty(max_out, dtype=torch.complex64).pin_memory()
+    d_acc = torch.empty(max_acc, dtype=torch.complex64, device=dev)
+    d_out = torch.empty(max_out, dtype=torch.complex64, device=dev)
+    h_bits = [inputs[i][1].cpu().pin_memory() for i in range(len(cases))]
+    stream = torch.cuda.current_stream(dev)
+    h2d = d2h = 0
+    for r, k, n, B in cases:
+        h2d += B * 2 ** r * 4 ** k * 8 + B * 4
+        d2h += B * 2 ** r * 4 ** n * 8
+
+    def step():
+        for ci, (r, k, n, B) in enumerate(cases):
+            variants, bits, site = inputs[ci]
+            na, no = B * 2 ** r * 4 ** k, B * 2 ** r * 4 ** n
+            d_acc[:na].copy_(h_acc[:na], non_blocking=True)
+            bits.copy_(h_bits[ci], non_blocking=True)
+            project_variants(variants, bits, site, 4 ** (k + n), stream)
+            plans[ci](d_acc, site, d_out, B, 2 ** r * 4 ** k, 4 ** (k + n), 2 ** r * 4 ** n, stream)
+            h_out[:no].copy_(d_out[:no], non_blocking=True)
+        torch.cuda.synchronize(dev)
+
+    step()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = max(1, min(args.steps, 3))
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    t = allreduce_max(e0.elapsed_time(e1) * 1e-3, world, dev)
+    units = sum(B for *_, B in cases) * steps * world
+    return {"value": units / t, "unit": "bitstring-steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "steps": steps, "path": "PairPlan + project_variants on host-resident pinned buffers"}
+
+
+def run_cfg0(args, rank, world, dev):
+    import torch
+
+    from paper_2011_02621_b200 import AmplitudeEngine, generate_lattice, pattern_rqc, square_patterns
+
+    g = generate_lattice("square", 3, 3)
+    circ = pattern_rqc(g, square_patterns(3, 3), 8, seed=0)
+    eng = AmplitudeEngine(circ, "0" * 9, dtype="complex128", device=dev)
+    rng = np.random.default_rng(rank)
+    B = 64
+    bits = rng.integers(0, 2, (B, 9)).astype(np.int32)
+    sel = eng.selectors(bits)
+    amp = torch.zeros(B, dtype=torch.complex128, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        eng.amplitudes_device(sel, B, amp)
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev.index) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            eng.amplitudes_device(sel, B, amp)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    t = allreduce_max(e0.elapsed_time(e1) * 1e-3, world, dev)
+    # e2e: host bitstrings in, host amplitudes out, through the public API
+    outs = ["".join(map(str, row)) for row in bits]
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        eng.amplitudes(outs)
+    te = allreduce_max(time.perf_counter() - t0, world, dev)
+    hbm, _, src = peaks()
+    return {"value": world * B * args.steps / t, "unit": "amplitudes/s", "ms_per_step": 1e3 * t / args.steps,
+            "gpu_launches": eng.executor.launches_per_chunk() * args.steps,
+            "roofline": {"bound": "latency", "achieved": None, "peak": hbm, "unit": "GB/s", "frac": None,
+                         "traffic": None, "note": "9-qubit network: launch-bound, see sweep workload"},
+            "config": {"workload": "configs[0] 3x3 square, 8 cycles, 64 bitstrings", "dtype": "complex128",
+                       "l2": "inputs L2-resident (tiny network)"},
+            "clocks": clk.summary(), "dtype": "complex128",
+            "e2e": {"value": world * B * args.steps / te, "unit": "amplitudes/s", "h2d_bytes_per_step": B * 9 * 4,
+                    "d2h_bytes_per_step": B * 16}}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm (oracle port of tnsim's numpy tensordot path)
+# ---------------------------------------------------------------------------
+def cpu_sweep_rates(budget_s: float = 20.0):
+    """Per-(k, n) CPU throughput (bytes/s of algorithmic traffic) of the
+    oracle port, measured on r = 16..20, B = 1 cases within ``budget_s``."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import tn_oracle as O
+
+    try:
+        from threadpoolctl import threadpool_info
+
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        threads = os.cpu_count() or 1
+    rng = np.random.default_rng(0)
+    rates = {}
+    t_start = time.perf_counter()
+    per_class = budget_s / 9
+    for k in (1, 2, 3):
+        for n in (1, 2, 3):
+            r = 18
+            perm, dims, pairs = case_layout(r, k, n, seed=k * 10 + n)
+            acc = (rng.standard_normal((1, 2 ** r * 4 ** k)) + 1j * rng.standard_normal((1, 2 ** r * 4 ** k))).astype(np.complex64)
+            site = (rng.standard_normal((2,) + (4,) * (k + n)) + 1j * rng.standard_normal((2,) + (4,) * (k + n))).astype(np.complex64)
+            bits = np.zeros(1, dtype=np.int64)
+            reps, t0 = 0, time.perf_counter()
+            while True:
+                O.sweep_step(acc, perm, r, k, site, bits)
+                reps += 1
+                el = time.perf_counter() - t0
+                if el > per_class or reps >= 50:
+                    break
+            by, _ = case_traffic(r, k, n, 1)
+            rates[(k, n)] = by * reps / el
+    return rates, threads, time.perf_counter() - t_start
+
+
+def cpu_value_for(cases, rates):
+    t = sum(case_traffic(*c)[0] / rates[(c[1], c[2])] for c in cases)
+    return sum(c[3] for c in cases) / t
+
+
+def run_reference(args):
+    rates, threads, spent = cpu_sweep_rates(args.cpu_budget)
+    cases = sweep_cases(args.limit)
+    v = cpu_value_for(cases, rates)
+    return v, threads, spent
+
+
+# ---------------------------------------------------------------------------
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def allreduce_max(x, world, dev):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="sweep", choices=["sweep", "cfg0"])
+    ap.add_argument("--limit", type=int, default=SWEEP_LIMIT)
+    ap.add_argument("--no-e2e", dest="e2e", action="store_false")
+    ap.add_argument("--no-cpu", dest="cpu", action="store_false")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    base = {"metric": METRIC, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "data": "synthetic (seeded)"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        v, threads, spent = run_reference(args)
+        line = dict(base, impl="reference", value=v, unit="bitstring-steps/s", n_gpus=world, dtype="complex64",
+                    ms_per_step=1e3 * sum(c[3] for c in sweep_cases(args.limit)) / v,
+                    config={"workload": "configs[1] pairwise-contraction sweep", "dtype": "complex64"},
+                    cpu_baseline={"value": v, "unit": "bitstring-steps/s", "cores": threads, "kind": "port",
+                                  "sample": f"oracle sweep_step (numpy tensordot) at r=18, B=1 for every (k,n); "
+                                            f"{spent:.1f}s of CPU; scaled per case by algorithmic bytes"},
+                    e2e={"value": v, "unit": "bitstring-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
+        print(json.dumps(line))
+        return
+
+    import torch
+
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    from paper_2011_02621_b200 import _native
+
+    _native.require_device()
+    res = run_sweep(args, rank, world, dev) if args.workload == "sweep" else run_cfg0(args, rank, world, dev)
+    if rank == 0:
+        if args.cpu and world == 1:
+            if args.workload == "sweep":
+                rates, threads, spent = cpu_sweep_rates(args.cpu_budget)
+                cv = cpu_value_for(sweep_cases(args.limit), rates)
+                res["cpu_baseline"] = {"value": cv, "unit": "bitstring-steps/s", "cores": threads, "kind": "port",
+                                       "sample": f"oracle sweep_step (numpy) r=18, B=1 per (k,n), {spent:.1f}s; "
+                                                 "scaled per case by algorithmic bytes"}
+        detail = res.pop("detail", None)
+        line = dict(base, **res)
+        print(json.dumps(line))
+        if detail is not None:
+            (ROOT / "gpurun_out").mkdir(exist_ok=True)
+            (ROOT / "gpurun_out" / "bench_detail.json").write_text(json.dumps(detail, indent=1))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -169,6 +169,20 @@ int  tnc_contract_pair(int dtype, int64_t batch,
                        void* out, int64_t out_zstride,
                        void* workspace, size_t workspace_bytes, void* stream);
 
+/* Reusable pairwise plan: the layout analysis and offset tables of
+ * tnc_contract_pair computed once (device tables owned by the plan), so a path
+ * step or a benchmark loop launches only the kernel.  Execute is asynchronous
+ * on `stream`. */
+typedef struct tnc_pair_plan tnc_pair_plan;
+int  tnc_pair_plan_create(int dtype, int a_rank, const int64_t* a_dims, int b_rank, const int64_t* b_dims,
+                          int npairs, const int32_t* pair_a, const int32_t* pair_b,
+                          const int32_t* out_perm, int conj_b, tnc_pair_plan** plan);
+int  tnc_pair_plan_execute(const tnc_pair_plan* plan, int64_t batch,
+                           const void* a, int64_t a_zstride, const void* b, int64_t b_zstride,
+                           void* out, int64_t out_zstride, void* stream);
+int  tnc_pair_plan_kernel(const tnc_pair_plan* plan);   /* TNC_K_SKINNY (tiled) or TNC_K_GENERIC */
+void tnc_pair_plan_destroy(tnc_pair_plan* plan);
+
 #ifdef __cplusplus
 }
 #endif

@@ -24,6 +24,7 @@ EXPORTS = (
     "tnc_version", "tnc_struct_size", "tnc_device_check", "tnc_last_error",
     "tnc_project", "tnc_step", "tnc_slice_sum", "tnc_contract_path",
     "tnc_contract_pair_workspace", "tnc_contract_pair",
+    "tnc_pair_plan_create", "tnc_pair_plan_execute", "tnc_pair_plan_kernel", "tnc_pair_plan_destroy",
 )
 
 
@@ -109,6 +110,16 @@ def lib():
         C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
         C.c_void_p, C.c_int64, C.c_void_p, C.c_size_t, C.c_void_p,
     ]
+    L.tnc_pair_plan_create.restype = C.c_int
+    L.tnc_pair_plan_create.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int,
+                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]
+    L.tnc_pair_plan_execute.restype = C.c_int
+    L.tnc_pair_plan_execute.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                        C.c_void_p, C.c_int64, C.c_void_p]
+    L.tnc_pair_plan_kernel.restype = C.c_int
+    L.tnc_pair_plan_kernel.argtypes = [C.c_void_p]
+    L.tnc_pair_plan_destroy.restype = None
+    L.tnc_pair_plan_destroy.argtypes = [C.c_void_p]
     for i, cls in enumerate((Site, StepDesc, ProjectDesc, SliceSumDesc, PathDesc)):
         native = L.tnc_struct_size(i)
         if native != C.sizeof(cls):

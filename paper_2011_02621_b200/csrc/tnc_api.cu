@@ -5,6 +5,7 @@
 #include <stdarg.h>
 #include <stdio.h>
 #include <string.h>
+#include <algorithm>
 #include <string>
 #include <vector>
 #include "tnc_kernels.cuh"
@@ -139,10 +140,61 @@ int launch_tiled_fn(KFN kern, const tnc::PairTile& p, int64_t batch, const void*
   return check_launch("tnc_contract_pair[tiled]");
 }
 
+template <typename R, typename KFN>
+int launch_pipe_fn(KFN kern, const tnc::PairTile& p, int64_t batch, const void* a, const void* b, void* out,
+                   cudaStream_t s, bool cols = false) {
+  using C = typename tnc::cplx<R>::T;
+  const size_t smem = cols ? 128 + (size_t)tnc::PIPE_STAGES * p.Kout * p.Lseg * sizeof(C) + (size_t)64 * 4 + (size_t)p.R * 4 + 16
+                           : 128 + (size_t)tnc::PIPE_STAGES * p.Kout * p.Lseg * sizeof(C)
+                             + (size_t)p.K * (p.N + 1) * sizeof(C) + (size_t)p.K * 4 + 16;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return check_launch("tnc pair pipe: smem attribute");
+  const int64_t total = batch * p.U;
+  if (total <= 0) return TNC_OK;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t ctas = std::min<int64_t>(total, (int64_t)sms * per_sm);
+  const int64_t per = (total + ctas - 1) / ctas;
+  const int64_t grid = (total + per - 1) / per;
+  kern<<<(unsigned)grid, 256, smem, s>>>(p, a, b, out, total, per);
+  return check_launch("tnc_contract_pair[pipe]");
+}
+
+bool pipe_eligible(const tnc::PairTile& p, size_t elem, const void* a) {
+  if ((p.Lseg * elem) % 16 != 0 || (p.a_zstride * elem) % 16 != 0 || ((uintptr_t)a) % 16 != 0) return false;
+  for (int j = 0; j < p.nfo; ++j) if ((p.fo_stride[j] * elem) % 16 != 0) return false;
+  return true;   // segoff are sums of outer strides, multiples of Lseg
+}
+
 template <typename R>
 int launch_pair_tiled(const tnc::PairTile& p, int64_t batch, const void* a, const void* b, void* out,
                       cudaStream_t s) {
+  using C = typename tnc::cplx<R>::T;
   const int64_t N = p.N, K = p.K;
+  if (p.pipe && pipe_eligible(p, sizeof(C), a)) {
+    if (N >= 8 && N <= 256 && (256 % N) == 0 && K <= (sizeof(R) == 4 ? 64 : 16)) {
+      if (K <= 4) return launch_pipe_fn<R>(tnc::k_pair_pipe_cols<R, 4>, p, batch, a, b, out, s, true);
+      if (K <= 16) return launch_pipe_fn<R>(tnc::k_pair_pipe_cols<R, 16>, p, batch, a, b, out, s, true);
+      if constexpr (sizeof(R) == 4) return launch_pipe_fn<R>(tnc::k_pair_pipe_cols<R, 64>, p, batch, a, b, out, s, true);
+    }
+    if (N <= 32) {
+      if (N <= 1) return launch_pipe_fn<R>(tnc::k_pair_pipe<R, 1, 0>, p, batch, a, b, out, s);
+      if (N <= 2) return launch_pipe_fn<R>(tnc::k_pair_pipe<R, 2, 0>, p, batch, a, b, out, s);
+      if (N <= 4) return launch_pipe_fn<R>(tnc::k_pair_pipe<R, 4, 0>, p, batch, a, b, out, s);
+      if (N <= 8) return launch_pipe_fn<R>(tnc::k_pair_pipe<R, 8, 0>, p, batch, a, b, out, s);
+      if (N <= 16) return launch_pipe_fn<R>(tnc::k_pair_pipe<R, 16, 0>, p, batch, a, b, out, s);
+      return launch_pipe_fn<R>(tnc::k_pair_pipe<R, 32, 0>, p, batch, a, b, out, s);
+    }
+    if (K <= 1) return launch_pipe_fn<R>(tnc::k_pair_pipe<R, 1, 1>, p, batch, a, b, out, s);
+    if (K <= 2) return launch_pipe_fn<R>(tnc::k_pair_pipe<R, 1, 2>, p, batch, a, b, out, s);
+    if (K <= 4) return launch_pipe_fn<R>(tnc::k_pair_pipe<R, 1, 4>, p, batch, a, b, out, s);
+    if (K <= 8) return launch_pipe_fn<R>(tnc::k_pair_pipe<R, 1, 8>, p, batch, a, b, out, s);
+    return launch_pipe_fn<R>(tnc::k_pair_pipe<R, 1, 16>, p, batch, a, b, out, s);
+  }
   if (N <= 32) {
     if (N <= 1) return launch_tiled_fn<R>(tnc::k_pair_tiled_acc<R, 1>, p, batch, a, b, out, s);
     if (N <= 2) return launch_tiled_fn<R>(tnc::k_pair_tiled_acc<R, 2>, p, batch, a, b, out, s);
@@ -222,12 +274,29 @@ int tnc_contract_path(const tnc_path_desc* d, void* stream) {
 }
 
 // ---------------------------------------------------------------------------
-// contract_pair: builds a one-step descriptor on the host, stages its offset
-// tables into the caller's device workspace and runs tnc_step.
+// Pairwise contraction plans (tensor.py:103 contract_pair).  The host side
+// computes the layout once -- which kernel, its tile geometry and offset
+// tables -- into one byte blob; the blob lives either in caller workspace
+// (one-shot tnc_contract_pair) or in plan-owned device memory.
 // ---------------------------------------------------------------------------
-static void pair_layout(int a_rank, const int64_t* a_dims, int b_rank, const int64_t* b_dims,
-                        int npairs, const int32_t* pa, const int32_t* pb,
-                        std::vector<int>& fa, std::vector<int>& fb, int64_t& K, int64_t& N) {
+}  // extern "C"
+
+struct tnc_pair_plan {
+  int dtype = 0;
+  int kind = TNC_K_GENERIC;        // TNC_K_GENERIC or TNC_K_SKINNY (tiled)
+  tnc_step_desc d;                 // generic launch template (tables patched)
+  tnc::PairTile pt;                // tiled launch template (tables patched)
+  std::vector<unsigned char> blob; // host copy of the tables
+  size_t o_ak = 0, o_bk = 0, o_bn = 0, o_cn = 0, o_seg = 0, o_row = 0, o_k = 0;
+  void* dmem = nullptr;            // plan-owned device copy (plan API)
+  bool a_align_needed = false;     // tiled vec16 requires 16-byte aligned a
+};
+
+namespace {
+
+void pair_layout(int a_rank, const int64_t* a_dims, int b_rank, const int64_t* b_dims,
+                 int npairs, const int32_t* pa, const int32_t* pb,
+                 std::vector<int>& fa, std::vector<int>& fb, int64_t& K, int64_t& N) {
   std::vector<char> ua(a_rank, 0), ub(b_rank, 0);
   for (int i = 0; i < npairs; ++i) { ua[pa[i]] = 1; ub[pb[i]] = 1; }
   fa.clear(); fb.clear();
@@ -238,25 +307,13 @@ static void pair_layout(int a_rank, const int64_t* a_dims, int b_rank, const int
   for (int i : fb) N *= b_dims[i];
 }
 
-size_t tnc_contract_pair_workspace(int a_rank, const int64_t* a_dims, int b_rank, const int64_t* b_dims,
-                                   int npairs, const int32_t* pair_a, const int32_t* pair_b) {
-  std::vector<int> fa, fb;
-  int64_t K, N;
-  pair_layout(a_rank, a_dims, b_rank, b_dims, npairs, pair_a, pair_b, fa, fb, K, N);
-  // generic tables + tiled-kernel tables (segoff <= K int64, rowoff <= 8192 int32, koff K int32)
-  return (size_t)(2 * K + 2 * N) * sizeof(int64_t) + (size_t)K * 8 + 8192 * 4 + (size_t)K * 4 + 256;
-}
-
-int tnc_contract_pair(int dtype, int64_t batch,
-                      const void* a, int a_rank, const int64_t* a_dims, int64_t a_zstride,
-                      const void* b, int b_rank, const int64_t* b_dims, int64_t b_zstride,
-                      int npairs, const int32_t* pair_a, const int32_t* pair_b,
-                      const int32_t* out_perm, int conj_b,
-                      void* out, int64_t out_zstride,
-                      void* workspace, size_t workspace_bytes, void* stream) {
-  if (!dtype_ok(dtype)) return fail(TNC_E_INVALID, "tnc_contract_pair: bad dtype %d", dtype);
+int build_pair_plan(tnc_pair_plan& P, int dtype, int a_rank, const int64_t* a_dims, int b_rank,
+                    const int64_t* b_dims, int npairs, const int32_t* pair_a, const int32_t* pair_b,
+                    const int32_t* out_perm, int conj_b) {
+  if (!dtype_ok(dtype)) return fail(TNC_E_INVALID, "contract_pair: bad dtype %d", dtype);
   if (a_rank < 0 || b_rank < 0 || a_rank > TNC_MAX_LEGS || b_rank > TNC_MAX_LEGS)
-    return fail(TNC_E_INVALID, "tnc_contract_pair: rank out of range");
+    return fail(TNC_E_INVALID, "contract_pair: rank out of range");
+  if (npairs < 0 || npairs > a_rank || npairs > b_rank) return fail(TNC_E_INVALID, "contract_pair: bad npairs");
   std::vector<char> ua(a_rank, 0), ub(b_rank, 0);
   for (int i = 0; i < npairs; ++i) {
     if (pair_a[i] < 0 || pair_a[i] >= a_rank || pair_b[i] < 0 || pair_b[i] >= b_rank)
@@ -266,16 +323,14 @@ int tnc_contract_pair(int dtype, int64_t batch,
     if (a_dims[pair_a[i]] != b_dims[pair_b[i]])
       return fail(TNC_E_INVALID, "extent mismatch on pair (%d, %d)", pair_a[i], pair_b[i]);
   }
+  for (int i = 0; i < a_rank; ++i) if (a_dims[i] < 1) return fail(TNC_E_INVALID, "axis extent < 1");
+  for (int i = 0; i < b_rank; ++i) if (b_dims[i] < 1) return fail(TNC_E_INVALID, "axis extent < 1");
   std::vector<int> fa, fb;
   int64_t K, N;
   pair_layout(a_rank, a_dims, b_rank, b_dims, npairs, pair_a, pair_b, fa, fb, K, N);
-  if (workspace_bytes < (size_t)(2 * K + 2 * N) * sizeof(int64_t))
-    return fail(TNC_E_INVALID, "tnc_contract_pair: workspace too small");
-  // row-major strides of a and b
   std::vector<int64_t> sa(a_rank), sb(b_rank);
   { int64_t s = 1; for (int i = a_rank - 1; i >= 0; --i) { sa[i] = s; s *= a_dims[i]; } }
   { int64_t s = 1; for (int i = b_rank - 1; i >= 0; --i) { sb[i] = s; s *= b_dims[i]; } }
-  // output axes: free a then free b, permuted by out_perm
   const int nout = (int)(fa.size() + fb.size());
   std::vector<int64_t> odims(nout);
   for (size_t i = 0; i < fa.size(); ++i) odims[i] = a_dims[fa[i]];
@@ -284,31 +339,14 @@ int tnc_contract_pair(int dtype, int64_t batch,
   for (int i = 0; i < nout; ++i) perm[i] = out_perm ? out_perm[i] : i;
   std::vector<char> seen(nout, 0);
   for (int i = 0; i < nout; ++i) {
-    if (perm[i] < 0 || perm[i] >= nout || seen[perm[i]]) return fail(TNC_E_INVALID, "tnc_contract_pair: bad out_perm");
+    if (perm[i] < 0 || perm[i] >= nout || seen[perm[i]]) return fail(TNC_E_INVALID, "contract_pair: bad out_perm");
     seen[perm[i]] = 1;
   }
-  std::vector<int64_t> ostride_by_src(nout);  // stride in out of natural axis j
-  { int64_t s = 1; for (int i = nout - 1; i >= 0; --i) { ostride_by_src[perm[i]] = s; s *= odims[perm[i]]; } }
+  std::vector<int64_t> ostr(nout);  // out stride of natural axis j
+  { int64_t s = 1; for (int i = nout - 1; i >= 0; --i) { ostr[perm[i]] = s; s *= odims[perm[i]]; } }
 
-  tnc_step_desc d;
-  memset(&d, 0, sizeof d);
-  d.dtype = dtype;
-  d.kernel = TNC_K_GENERIC;
-  d.Z = batch;
-  d.slices_per_b = 1;
-  d.acc = a; d.acc_zstride = a_zstride;
-  d.out = out; d.out_zstride = out_zstride;
-  d.site.ptr = b; d.site.zstride = b_zstride;
-  d.conj_b = conj_b ? 1 : 0;
-  d.nf = (int)fa.size();
-  d.M = 1;
-  for (size_t i = 0; i < fa.size(); ++i) {
-    d.f_dim[i] = a_dims[fa[i]];
-    d.f_astride[i] = sa[fa[i]];
-    d.f_cstride[i] = ostride_by_src[i];
-    d.M *= a_dims[fa[i]];
-  }
-  d.K = K; d.N = N;
+  P.dtype = dtype;
+  // generic tables: a_koff[K], b_koff[K], b_noff[N], c_noff[N]
   std::vector<int64_t> tab(2 * K + 2 * N);
   for (int64_t k = 0; k < K; ++k) {
     int64_t r = k, oa = 0, ob = 0;
@@ -325,34 +363,48 @@ int tnc_contract_pair(int dtype, int64_t batch,
     for (int i = (int)fb.size() - 1; i >= 0; --i) {
       const int64_t dm = b_dims[fb[i]];
       obn += (r % dm) * sb[fb[i]];
-      ocn += (r % dm) * ostride_by_src[fa.size() + i];
+      ocn += (r % dm) * ostr[fa.size() + i];
       r /= dm;
     }
     tab[2 * K + n] = obn; tab[2 * K + N + n] = ocn;
   }
-  cudaStream_t s = (cudaStream_t)stream;
-  bool identity_a = true;  // free a legs keep their order at the front of out
+  tnc_step_desc& d = P.d;
+  memset(&d, 0, sizeof d);
+  d.dtype = dtype;
+  d.kernel = TNC_K_GENERIC;
+  d.slices_per_b = 1;
+  d.conj_b = conj_b ? 1 : 0;
+  d.nf = (int)fa.size();
+  d.M = 1;
+  for (size_t i = 0; i < fa.size(); ++i) {
+    d.f_dim[i] = a_dims[fa[i]];
+    d.f_astride[i] = sa[fa[i]];
+    d.f_cstride[i] = ostr[i];
+    d.M *= a_dims[fa[i]];
+  }
+  d.K = K; d.N = N;
+
+  bool identity_a = true;
   for (size_t i = 0; i < fa.size(); ++i) identity_a = identity_a && perm[i] == (int)i;
-  const int64_t tile_max = dtype == TNC_C64 ? 8192 : 4096;
-  const bool tiled_ok = identity_a && K * N <= 4096 && (N <= 32 || K <= 16) && a_rank > 0;
-  if (tiled_ok) {
+  const int64_t tile_max = dtype == TNC_C64 ? 4096 : 2048;   // one ring stage: 32 KiB
+  std::vector<int64_t> segoff;
+  std::vector<int32_t> rowoff, koff;
+  P.kind = TNC_K_GENERIC;
+  if (identity_a && K * N <= 4096 && (N <= 32 || K <= 16) && a_rank > 0) {
     std::vector<char> shared(a_rank, 0);
     for (int i = 0; i < npairs; ++i) shared[pair_a[i]] = 1;
-    // grow the segment from the innermost leg while the tile fits
     int t = a_rank;
     int64_t lseg = 1, kout = K;
     while (t > 0) {
-      const int64_t d = a_dims[t - 1];
-      const int64_t nl = lseg * d, nk = shared[t - 1] ? kout / d : kout;
+      const int64_t dm = a_dims[t - 1];
+      const int64_t nl = lseg * dm, nk = shared[t - 1] ? kout / dm : kout;
       if (nk * nl > tile_max) break;
       lseg = nl; kout = nk; --t;
     }
-    const int64_t tile = kout * lseg;
-    const int64_t R = tile / K;
+    const int64_t tile = kout * lseg, R = tile / K;
     if (tile <= tile_max && R >= 1) {
-      tnc::PairTile pt;
+      tnc::PairTile& pt = P.pt;
       memset(&pt, 0, sizeof pt);
-      // outer free legs / outer shared legs / inner free legs
       std::vector<int> of, os, inf;
       for (int i = 0; i < a_rank; ++i) {
         if (i < t) (shared[i] ? os : of).push_back(i);
@@ -361,18 +413,18 @@ int tnc_contract_pair(int dtype, int64_t batch,
       pt.nfo = (int)of.size();
       pt.U = 1;
       for (size_t j = 0; j < of.size(); ++j) { pt.fo_dim[j] = a_dims[of[j]]; pt.fo_stride[j] = sa[of[j]]; pt.U *= a_dims[of[j]]; }
-      pt.a_zstride = a_zstride; pt.b_zstride = b_zstride; pt.out_zstride = out_zstride;
       pt.conj_b = conj_b ? 1 : 0;
       pt.Kout = kout; pt.Lseg = lseg; pt.R = R; pt.K = K; pt.N = N;
-      std::vector<int64_t> segoff(kout);
-      std::vector<int64_t> segw(a_rank, 0);  // mixed-radix weight of an outer shared leg
+      segoff.resize(kout);
+      std::vector<int64_t> segw(a_rank, 0);
       { int64_t w = 1; for (int j = (int)os.size() - 1; j >= 0; --j) { segw[os[j]] = w; w *= a_dims[os[j]]; } }
       for (int64_t j = 0; j < kout; ++j) {
         int64_t r = j, off = 0;
         for (int q = (int)os.size() - 1; q >= 0; --q) { off += (r % a_dims[os[q]]) * sa[os[q]]; r /= a_dims[os[q]]; }
         segoff[j] = off;
       }
-      std::vector<int32_t> rowoff(R), koff(K);
+      rowoff.resize(R);
+      koff.resize(K);
       for (int64_t r0 = 0; r0 < R; ++r0) {
         int64_t r = r0, off = 0;
         for (int q = (int)inf.size() - 1; q >= 0; --q) { off += (r % a_dims[inf[q]]) * sa[inf[q]]; r /= a_dims[inf[q]]; }
@@ -388,43 +440,132 @@ int tnc_contract_pair(int dtype, int64_t batch,
         }
         koff[k0] = (int32_t)(seg * lseg + inner);
       }
-      bool v16 = dtype == TNC_C64 && (lseg % 2 == 0) && (a_zstride % 2 == 0) && (((uintptr_t)a) % 16 == 0);
+      bool v16 = dtype == TNC_C64 && (lseg % 2 == 0);
       for (int64_t j = 0; j < kout && v16; ++j) v16 = (segoff[j] % 2 == 0);
       pt.vec16 = v16 ? 1 : 0;
-      // workspace: [b_koff K][b_noff N] int64, segoff int64, rowoff int32, koff int32
-      unsigned char* w = reinterpret_cast<unsigned char*>(workspace);
-      size_t o_bk = 0, o_bn = o_bk + K * 8, o_seg = o_bn + N * 8, o_row = o_seg + kout * 8, o_k = o_row + R * 4;
-      const size_t total = o_k + K * 4;
-      if (total > workspace_bytes) return fail(TNC_E_INVALID, "tnc_contract_pair: workspace too small");
-      std::vector<unsigned char> blob(total);
-      memcpy(blob.data() + o_bk, tab.data() + K, K * 8);
-      memcpy(blob.data() + o_bn, tab.data() + 2 * K, N * 8);
-      memcpy(blob.data() + o_seg, segoff.data(), kout * 8);
-      memcpy(blob.data() + o_row, rowoff.data(), R * 4);
-      memcpy(blob.data() + o_k, koff.data(), K * 4);
-      if (cudaMemcpyAsync(workspace, blob.data(), total, cudaMemcpyHostToDevice, s) != cudaSuccess)
-        return check_launch("tnc_contract_pair: table upload");
-      pt.b_koff = reinterpret_cast<const int64_t*>(w + o_bk);
-      pt.b_noff = reinterpret_cast<const int64_t*>(w + o_bn);
-      pt.segoff = reinterpret_cast<const int64_t*>(w + o_seg);
-      pt.rowoff = reinterpret_cast<const int32_t*>(w + o_row);
-      pt.koff = reinterpret_cast<const int32_t*>(w + o_k);
-      int rc = dtype == TNC_C64 ? launch_pair_tiled<float>(pt, batch, a, b, out, s)
-                                : launch_pair_tiled<double>(pt, batch, a, b, out, s);
-      if (rc) return rc;
-      if (cudaStreamSynchronize(s) != cudaSuccess) return check_launch("tnc_contract_pair: sync");
-      return TNC_OK;
+      pt.pipe = 1;
+      P.a_align_needed = v16;
+      P.kind = TNC_K_SKINNY;
     }
   }
-  if (cudaMemcpyAsync(workspace, tab.data(), tab.size() * sizeof(int64_t), cudaMemcpyHostToDevice, s) != cudaSuccess)
-    return check_launch("tnc_contract_pair: table upload");
-  int64_t* w = reinterpret_cast<int64_t*>(workspace);
-  d.a_koff = w; d.b_koff = w + K; d.b_noff = w + 2 * K; d.c_noff = w + 2 * K + N;
-  int rc = tnc_step(&d, stream);
+  // blob layout (8-byte aligned sections)
+  size_t o = 0;
+  P.o_ak = o; o += K * 8;
+  P.o_bk = o; o += K * 8;
+  P.o_bn = o; o += N * 8;
+  P.o_cn = o; o += N * 8;
+  P.o_seg = o; o += segoff.size() * 8;
+  P.o_row = o; o += rowoff.size() * 4;
+  o = (o + 7) & ~(size_t)7;
+  P.o_k = o; o += koff.size() * 4;
+  P.blob.assign(o + 8, 0);
+  memcpy(P.blob.data() + P.o_ak, tab.data(), 2 * K * 8);                    // a_koff, b_koff
+  memcpy(P.blob.data() + P.o_bn, tab.data() + 2 * K, N * 8 * 2);             // b_noff, c_noff
+  if (!segoff.empty()) memcpy(P.blob.data() + P.o_seg, segoff.data(), segoff.size() * 8);
+  if (!rowoff.empty()) memcpy(P.blob.data() + P.o_row, rowoff.data(), rowoff.size() * 4);
+  if (!koff.empty()) memcpy(P.blob.data() + P.o_k, koff.data(), koff.size() * 4);
+  return TNC_OK;
+}
+
+void bind_tables(tnc_pair_plan& P, void* dev) {
+  unsigned char* w = reinterpret_cast<unsigned char*>(dev);
+  P.d.a_koff = reinterpret_cast<const int64_t*>(w + P.o_ak);
+  P.d.b_koff = reinterpret_cast<const int64_t*>(w + P.o_bk);
+  P.d.b_noff = reinterpret_cast<const int64_t*>(w + P.o_bn);
+  P.d.c_noff = reinterpret_cast<const int64_t*>(w + P.o_cn);
+  P.pt.b_koff = P.d.b_koff;
+  P.pt.b_noff = P.d.b_noff;
+  P.pt.segoff = reinterpret_cast<const int64_t*>(w + P.o_seg);
+  P.pt.rowoff = reinterpret_cast<const int32_t*>(w + P.o_row);
+  P.pt.koff = reinterpret_cast<const int32_t*>(w + P.o_k);
+}
+
+int execute_pair_plan(const tnc_pair_plan& P, int64_t batch, const void* a, int64_t a_zstride, const void* b,
+                      int64_t b_zstride, void* out, int64_t out_zstride, cudaStream_t s) {
+  if (batch <= 0) return TNC_OK;
+  if (P.kind == TNC_K_SKINNY) {
+    tnc::PairTile pt = P.pt;
+    pt.a_zstride = a_zstride; pt.b_zstride = b_zstride; pt.out_zstride = out_zstride;
+    if (pt.vec16 && ((((uintptr_t)a) % 16) != 0 || (a_zstride % 2) != 0)) pt.vec16 = 0;
+    return P.dtype == TNC_C64 ? launch_pair_tiled<float>(pt, batch, a, b, out, s)
+                              : launch_pair_tiled<double>(pt, batch, a, b, out, s);
+  }
+  tnc_step_desc d = P.d;
+  d.Z = batch;
+  d.acc = a; d.acc_zstride = a_zstride;
+  d.out = out; d.out_zstride = out_zstride;
+  d.site.ptr = b; d.site.zstride = b_zstride;
+  return tnc_step(&d, (void*)s);
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t tnc_contract_pair_workspace(int a_rank, const int64_t* a_dims, int b_rank, const int64_t* b_dims,
+                                   int npairs, const int32_t* pair_a, const int32_t* pair_b) {
+  std::vector<int> fa, fb;
+  int64_t K, N;
+  pair_layout(a_rank, a_dims, b_rank, b_dims, npairs, pair_a, pair_b, fa, fb, K, N);
+  return (size_t)(2 * K + 2 * N) * 8 + (size_t)K * 8 + 8192 * 4 + (size_t)K * 4 + 64;
+}
+
+int tnc_contract_pair(int dtype, int64_t batch,
+                      const void* a, int a_rank, const int64_t* a_dims, int64_t a_zstride,
+                      const void* b, int b_rank, const int64_t* b_dims, int64_t b_zstride,
+                      int npairs, const int32_t* pair_a, const int32_t* pair_b,
+                      const int32_t* out_perm, int conj_b,
+                      void* out, int64_t out_zstride,
+                      void* workspace, size_t workspace_bytes, void* stream) {
+  tnc_pair_plan P;
+  int rc = build_pair_plan(P, dtype, a_rank, a_dims, b_rank, b_dims, npairs, pair_a, pair_b, out_perm, conj_b);
   if (rc) return rc;
-  // tab must stay alive until the async copy has consumed it
+  if (workspace_bytes < P.blob.size()) return fail(TNC_E_INVALID, "tnc_contract_pair: workspace too small");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemcpyAsync(workspace, P.blob.data(), P.blob.size(), cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return check_launch("tnc_contract_pair: table upload");
+  bind_tables(P, workspace);
+  rc = execute_pair_plan(P, batch, a, a_zstride, b, b_zstride, out, out_zstride, s);
+  if (rc) return rc;
+  // the host blob must outlive the async upload
   if (cudaStreamSynchronize(s) != cudaSuccess) return check_launch("tnc_contract_pair: sync");
   return TNC_OK;
+}
+
+int tnc_pair_plan_create(int dtype, int a_rank, const int64_t* a_dims, int b_rank, const int64_t* b_dims,
+                         int npairs, const int32_t* pair_a, const int32_t* pair_b,
+                         const int32_t* out_perm, int conj_b, tnc_pair_plan** plan) {
+  if (!plan) return fail(TNC_E_INVALID, "tnc_pair_plan_create: null plan pointer");
+  *plan = nullptr;
+  tnc_pair_plan* P = new tnc_pair_plan();
+  int rc = build_pair_plan(*P, dtype, a_rank, a_dims, b_rank, b_dims, npairs, pair_a, pair_b, out_perm, conj_b);
+  if (rc) { delete P; return rc; }
+  if (cudaMalloc(&P->dmem, P->blob.size()) != cudaSuccess) {
+    delete P;
+    return check_launch("tnc_pair_plan_create: cudaMalloc");
+  }
+  if (cudaMemcpy(P->dmem, P->blob.data(), P->blob.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(P->dmem);
+    delete P;
+    return check_launch("tnc_pair_plan_create: upload");
+  }
+  bind_tables(*P, P->dmem);
+  *plan = P;
+  return TNC_OK;
+}
+
+int tnc_pair_plan_execute(const tnc_pair_plan* plan, int64_t batch, const void* a, int64_t a_zstride,
+                          const void* b, int64_t b_zstride, void* out, int64_t out_zstride, void* stream) {
+  if (!plan) return fail(TNC_E_INVALID, "tnc_pair_plan_execute: null plan");
+  return execute_pair_plan(*plan, batch, a, a_zstride, b, b_zstride, out, out_zstride, (cudaStream_t)stream);
+}
+
+int tnc_pair_plan_kernel(const tnc_pair_plan* plan) { return plan ? plan->kind : TNC_E_INVALID; }
+
+void tnc_pair_plan_destroy(tnc_pair_plan* plan) {
+  if (!plan) return;
+  if (plan->dmem) cudaFree(plan->dmem);
+  delete plan;
 }
 
 }  // extern "C"

@@ -23,7 +23,7 @@ struct PairTile {
   const int64_t* b_koff;       // [K]
   const int64_t* b_noff;       // [N]
   int32_t vec16;               // segment base offsets and Lseg allow 16-byte copies
-  int32_t _pad;
+  int32_t pipe;                // use the pipelined persistent kernel when alignment allows
 };
 
 template <typename C>
@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(256)
 k_pair_tiled_acc(const __grid_constant__ PairTile p, const void* __restrict__ A_, const void* __restrict__ B_,
                  void* __restrict__ O_) {
   using C = typename cplx<R>::T;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   C* tile = reinterpret_cast<C*>(smem_raw);
   C* S = tile + p.Kout * p.Lseg;
   int32_t* koff_s = reinterpret_cast<int32_t*>(S + p.K * p.N);
@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(256)
 k_pair_tiled_row(const __grid_constant__ PairTile p, const void* __restrict__ A_, const void* __restrict__ B_,
                  void* __restrict__ O_) {
   using C = typename cplx<R>::T;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   C* tile = reinterpret_cast<C*>(smem_raw);
   C* S = tile + p.Kout * p.Lseg;
   int32_t* koff_s = reinterpret_cast<int32_t*>(S + p.K * p.N);
@@ -161,6 +161,211 @@ k_pair_tiled_row(const __grid_constant__ PairTile p, const void* __restrict__ A_
           if (n0 + j < N) orow[n0 + j] = acc[j];
       }
     }
+  }
+}
+
+}  // namespace tnc
+
+namespace tnc {
+
+// ---------------------------------------------------------------------------
+// Pipelined persistent version: each CTA walks a contiguous range of tiles;
+// thread 0 streams the next tiles' K_out segments into a 2-stage ring with
+// cp.async.bulk (TMA 1-D, mbarrier completion) while all threads contract the
+// current tile.  Shared-k reads are lane-rotated ((k + lane) % K) and the site
+// block is stored with an odd row pitch, so both smem streams are
+// conflict-free for the power-of-two extents of lattice networks.
+// ---------------------------------------------------------------------------
+constexpr int PIPE_STAGES = 2;
+
+template <typename C>
+__device__ __forceinline__ void issue_tile(const PairTile& p, const C* A, int64_t t, C* dst, uint64_t* bar) {
+  const int64_t z = t / p.U, u = t - (t / p.U) * p.U;
+  const int64_t base = tile_base(p, z, u);
+  const uint32_t seg_bytes = (uint32_t)(p.Lseg * sizeof(C));
+  mbar_expect_tx(bar, (uint32_t)(p.Kout * seg_bytes));
+  for (int64_t j = 0; j < p.Kout; ++j) bulk_g2s(dst + j * p.Lseg, A + base + p.segoff[j], seg_bytes, bar);
+}
+
+template <typename R, int NMAX, int KMAX>
+__global__ void __launch_bounds__(256, 2)
+k_pair_pipe(const __grid_constant__ PairTile p, const void* __restrict__ A_, const void* __restrict__ B_,
+            void* __restrict__ O_, int64_t tiles_total, int64_t tiles_per_cta) {
+  using C = typename cplx<R>::T;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
+  C* ring = reinterpret_cast<C*>(smem_raw + 128);
+  const int64_t tile_elems = p.Kout * p.Lseg;
+  const int SP = (int)p.N + 1;
+  C* S = ring + PIPE_STAGES * tile_elems;
+  int32_t* koff_s = reinterpret_cast<int32_t*>(S + p.K * SP);
+  const C* A = reinterpret_cast<const C*>(A_);
+  const C* B = reinterpret_cast<const C*>(B_);
+  C* O = reinterpret_cast<C*>(O_);
+  const int64_t t0 = blockIdx.x * tiles_per_cta;
+  const int64_t t1 = min(t0 + tiles_per_cta, tiles_total);
+  if (t0 >= t1) return;
+  const int K = (int)p.K, N = (int)p.N;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < PIPE_STAGES; ++s) mbar_init(&bars[s], 1);
+    mbar_fence_init();
+  }
+  for (int k = threadIdx.x; k < K; k += blockDim.x) koff_s[k] = p.koff[k];
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int s = 0; s < PIPE_STAGES && t0 + s < t1; ++s) issue_tile<C>(p, A, t0 + s, ring + s * tile_elems, &bars[s]);
+  int64_t cur_z = -1;
+  const int rot = (K >= 8) ? lane % K : 0;   // lane-rotated start in the shared index
+  for (int64_t i = 0; t0 + i < t1; ++i) {
+    const int64_t t = t0 + i;
+    const int stage = (int)(i % PIPE_STAGES);
+    const uint32_t phase = (uint32_t)((i / PIPE_STAGES) & 1);
+    const int64_t z = t / p.U, u = t - (t / p.U) * p.U;
+    if (z != cur_z) {
+      __syncthreads();
+      const C* Bz = B + z * p.b_zstride;
+      for (int64_t e = threadIdx.x; e < p.K * p.N; e += blockDim.x) {
+        const int64_t k = e / p.N, n = e - k * p.N;
+        C v = __ldg(Bz + p.b_koff[k] + p.b_noff[n]);
+        if (p.conj_b) v = cconj(v);
+        S[k * SP + n] = v;
+      }
+      __syncthreads();
+      cur_z = z;
+    }
+    mbar_wait(&bars[stage], phase);
+    const C* tile = ring + stage * tile_elems;
+    C* Ot = O + z * p.out_zstride + u * p.R * p.N;
+    for (int64_t r = threadIdx.x; r < p.R; r += blockDim.x) {
+      const C* trow = tile + p.rowoff[r];
+      C* orow = Ot + r * N;
+      if constexpr (KMAX == 0) {
+        // accumulator-resident: N <= NMAX outputs in registers
+        C acc[NMAX];
+#pragma unroll
+        for (int n = 0; n < NMAX; ++n) acc[n] = czero<R>();
+        int k = rot;
+        for (int kk = 0; kk < K; ++kk) {
+          const C a = trow[koff_s[k]];
+          const C* srow = S + k * SP;
+#pragma unroll
+          for (int n = 0; n < NMAX; ++n)
+            if (n < N) cfma(acc[n], a, srow[n]);
+          k = (k + 1 == K) ? 0 : k + 1;
+        }
+#pragma unroll
+        for (int n = 0; n < NMAX; ++n)
+          if (n < N) orow[n] = acc[n];
+      } else {
+        // row-resident: the row's K <= KMAX values in registers (rotated)
+        C av[KMAX];
+        int kidx[KMAX];
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j) {
+          int k = rot + j;
+          k = (k >= K) ? k - K : k;
+          kidx[j] = k;
+          av[j] = (j < K) ? trow[koff_s[j < K ? k : 0]] : czero<R>();
+        }
+        for (int n0 = 0; n0 < N; n0 += 8) {
+          C acc[8];
+#pragma unroll
+          for (int jn = 0; jn < 8; ++jn) acc[jn] = czero<R>();
+#pragma unroll
+          for (int j = 0; j < KMAX; ++j) {
+            if (j < K) {
+              const C* srow = S + kidx[j] * SP + n0;
+#pragma unroll
+              for (int jn = 0; jn < 8; ++jn)
+                if (n0 + jn < N) cfma(acc[jn], av[j], srow[jn]);
+            }
+          }
+#pragma unroll
+          for (int jn = 0; jn < 8; ++jn)
+            if (n0 + jn < N) orow[n0 + jn] = acc[jn];
+        }
+      }
+    }
+    __syncthreads();   // everyone is done with this stage
+    if (threadIdx.x == 0 && t + PIPE_STAGES < t1)
+      issue_tile<C>(p, A, t + PIPE_STAGES, ring + stage * tile_elems, &bars[stage]);
+  }
+}
+
+}  // namespace tnc
+
+namespace tnc {
+
+// ---------------------------------------------------------------------------
+// Element-mapped pipelined variant for N >= 8 (N | 256): consecutive threads
+// own consecutive *outputs* of the tile's contiguous [R][N] result block, so
+// stores are fully coalesced; a thread's output column n is fixed, its site
+// column S[:, n] lives in registers, and the accumulator values a[row][k] are
+// warp broadcasts (N >= 32) or few-way reads from the staged tile.
+// ---------------------------------------------------------------------------
+template <typename R, int KMAX>
+__global__ void __launch_bounds__(256, 1)
+k_pair_pipe_cols(const __grid_constant__ PairTile p, const void* __restrict__ A_, const void* __restrict__ B_,
+                 void* __restrict__ O_, int64_t tiles_total, int64_t tiles_per_cta) {
+  using C = typename cplx<R>::T;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
+  C* ring = reinterpret_cast<C*>(smem_raw + 128);
+  const int64_t tile_elems = p.Kout * p.Lseg;
+  int32_t* koff_s = reinterpret_cast<int32_t*>(ring + PIPE_STAGES * tile_elems);
+  int32_t* rowoff_s = koff_s + KMAX;
+  const C* A = reinterpret_cast<const C*>(A_);
+  const C* B = reinterpret_cast<const C*>(B_);
+  C* O = reinterpret_cast<C*>(O_);
+  const int64_t t0 = blockIdx.x * tiles_per_cta;
+  const int64_t t1 = min(t0 + tiles_per_cta, tiles_total);
+  if (t0 >= t1) return;
+  const int K = (int)p.K, N = (int)p.N;
+  const int Rr = (int)p.R;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < PIPE_STAGES; ++s) mbar_init(&bars[s], 1);
+    mbar_fence_init();
+  }
+  for (int k = threadIdx.x; k < K; k += blockDim.x) koff_s[k] = p.koff[k];
+  for (int r = threadIdx.x; r < Rr; r += blockDim.x) rowoff_s[r] = p.rowoff[r];
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int s = 0; s < PIPE_STAGES && t0 + s < t1; ++s) issue_tile<C>(p, A, t0 + s, ring + s * tile_elems, &bars[s]);
+  const int n = threadIdx.x % N;          // fixed output column of this thread
+  const int row_step = blockDim.x / N;
+  const int row0 = threadIdx.x / N;
+  C scol[KMAX];
+  int64_t cur_z = -1;
+  for (int64_t i = 0; t0 + i < t1; ++i) {
+    const int64_t t = t0 + i;
+    const int stage = (int)(i % PIPE_STAGES);
+    const uint32_t phase = (uint32_t)((i / PIPE_STAGES) & 1);
+    const int64_t z = t / p.U, u = t - (t / p.U) * p.U;
+    if (z != cur_z) {
+      const C* Bz = B + z * p.b_zstride + p.b_noff[n];
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k) {
+        C v = (k < K) ? __ldg(Bz + p.b_koff[k < K ? k : 0]) : czero<R>();
+        if (p.conj_b) v = cconj(v);
+        scol[k] = v;
+      }
+      cur_z = z;
+    }
+    mbar_wait(&bars[stage], phase);
+    const C* tile = ring + stage * tile_elems;
+    C* Ot = O + z * p.out_zstride + u * p.R * p.N;
+    for (int row = row0; row < Rr; row += row_step) {
+      const C* trow = tile + rowoff_s[row];
+      C acc = czero<R>();
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k)
+        if (k < K) cfma(acc, trow[koff_s[k]], scol[k]);
+      Ot[(int64_t)row * N + n] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && t + PIPE_STAGES < t1)
+      issue_tile<C>(p, A, t + PIPE_STAGES, ring + stage * tile_elems, &bars[stage]);
   }
 }
 

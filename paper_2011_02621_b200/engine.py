@@ -516,3 +516,85 @@ def device_contract_pair(a: np.ndarray, b: np.ndarray, pairs, out_perm=None, con
         odims = [odims[p] for p in out_perm]
     res = out[0].cpu().numpy().astype(np.complex128)
     return res.reshape(odims)
+
+
+class PairPlan:
+    """Reusable batched pairwise contraction (``tnc_pair_plan``): the layout
+    analysis and offset tables are built once; each call launches only the
+    kernel (asynchronously on the current stream)."""
+
+    def __init__(self, a_dims, b_dims, pairs, dtype: str = "complex64", out_perm=None, conj_b=False):
+        NV.require_device()
+        self.L = NV.lib()
+        self.code = dtype_code(dtype)
+        self.a_dims = [int(d) for d in a_dims]
+        self.b_dims = [int(d) for d in b_dims]
+        self.pairs = [tuple(p) for p in pairs]
+        adims = np.array(self.a_dims, dtype=np.int64)
+        bdims = np.array(self.b_dims, dtype=np.int64)
+        pa = np.array([p[0] for p in self.pairs], dtype=np.int32)
+        pb = np.array([p[1] for p in self.pairs], dtype=np.int32)
+        sa, sb = {p[0] for p in self.pairs}, {p[1] for p in self.pairs}
+        odims = [d for i, d in enumerate(self.a_dims) if i not in sa] + [d for i, d in enumerate(self.b_dims) if i not in sb]
+        perm = None
+        if out_perm is not None:
+            perm = np.array(list(out_perm), dtype=np.int32)
+            odims = [odims[p] for p in out_perm]
+        self.out_dims = odims
+        self.K = prod(self.a_dims[p[0]] for p in self.pairs) if self.pairs else 1
+        self.N = prod(odims[len(self.a_dims) - len(self.pairs):]) if odims else 1
+        h = C.c_void_p()
+        NV.check(self.L.tnc_pair_plan_create(self.code, len(adims), adims.ctypes.data, len(bdims), bdims.ctypes.data,
+                                             len(pa), pa.ctypes.data if len(pa) else None,
+                                             pb.ctypes.data if len(pb) else None,
+                                             perm.ctypes.data if perm is not None else None,
+                                             1 if conj_b else 0, C.byref(h)), "tnc_pair_plan_create")
+        self._h = h
+
+    @property
+    def kernel(self) -> str:
+        k = self.L.tnc_pair_plan_kernel(self._h)
+        return {NV.K_SKINNY: "tiled-permute", NV.K_GENERIC: "generic"}.get(k, str(k))
+
+    def __call__(self, a, b, out, batch: int, a_zstride: int, b_zstride: int, out_zstride: int, stream=None):
+        import torch
+
+        st = torch.cuda.current_stream() if stream is None else stream
+        NV.check(self.L.tnc_pair_plan_execute(self._h, batch, a.data_ptr(), a_zstride, b.data_ptr(), b_zstride,
+                                              out.data_ptr(), out_zstride, C.c_void_p(st.cuda_stream)),
+                 "tnc_pair_plan_execute")
+        return out
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                self.L.tnc_pair_plan_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+
+def project_variants(variants, bits, out, K_times_N: int, stream=None):
+    """Bitstring projection of a site: out[b] = variants[bits[b]] (tnc_project
+    gather).  variants: device [V, K*N]; bits: device int32 [B]."""
+    import torch
+
+    L = NV.lib()
+    code = NV.C64 if variants.dtype == torch.complex64 else NV.C128
+    d = NV.ProjectDesc()
+    d.dtype = code
+    d.conj = 0
+    d.Z = int(bits.numel())
+    d.slices_per_b = 1
+    d.s0 = 0
+    _fill_site(d.site, variants.data_ptr(), K_times_N, [])
+    d.site.sel = bits.data_ptr()
+    d.out = out.data_ptr()
+    d.out_zstride = K_times_N
+    d.nd = 1
+    d.dim[0] = K_times_N
+    d.src_stride[0] = 1
+    st = torch.cuda.current_stream() if stream is None else stream
+    NV.check(L.tnc_project(C.byref(d), C.c_void_p(st.cuda_stream)), "tnc_project")
+    return out
