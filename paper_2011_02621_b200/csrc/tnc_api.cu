@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 #include <algorithm>
 #include <string>
@@ -15,6 +16,16 @@
 namespace {
 
 thread_local std::string g_err;
+
+// TNC_KERNELS=simt disables the tensor-core path (tests compare both)
+bool tc_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TNC_KERNELS");
+    v = (e && strcmp(e, "simt") == 0) ? 0 : 1;
+  }
+  return v == 1;
+}
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -99,9 +110,10 @@ int launch_step(const tnc_step_desc& d, cudaStream_t s) {
   if (d.nf < 0 || d.nf > TNC_MAX_LEGS) return fail(TNC_E_INVALID, "tnc_step: nf=%d", d.nf);
   if (d.site.ncut < 0 || d.site.ncut > TNC_MAX_CUTS) return fail(TNC_E_INVALID, "tnc_step: ncut=%d", d.site.ncut);
   int kernel = d.kernel;
-  if (kernel == TNC_K_TC || kernel == TNC_K_AUTO) {
+  if (kernel == TNC_K_TC || (kernel == TNC_K_AUTO && tc_enabled())) {
     int rc = tnc::try_tc<R>(d, s);
     if (rc == 1) return check_launch("tnc_step[tc]");
+    if (rc < 0) return check_launch("tnc_step[tc] launch");
     if (kernel == TNC_K_TC) return fail(TNC_E_UNSUPPORTED, "tnc_step: shape outside the tensor-core kernel envelope");
   }
   if (kernel == TNC_K_SKINNY || kernel == TNC_K_AUTO) {
@@ -123,6 +135,7 @@ int launch_slice_sum(const tnc_slice_sum_desc& d, cudaStream_t s) {
 }
 
 bool dtype_ok(int dt) { return dt == TNC_C64 || dt == TNC_C128; }
+
 
 template <typename R, typename KFN>
 int launch_tiled_fn(KFN kern, const tnc::PairTile& p, int64_t batch, const void* a, const void* b, void* out,
@@ -290,6 +303,14 @@ struct tnc_pair_plan {
   size_t o_ak = 0, o_bk = 0, o_bn = 0, o_cn = 0, o_seg = 0, o_row = 0, o_k = 0;
   void* dmem = nullptr;            // plan-owned device copy (plan API)
   bool a_align_needed = false;     // tiled vec16 requires 16-byte aligned a
+  bool tc_ok = false;              // tensor-core kernel envelope (complex64)
+  tnc::TcDesc tc;                  // tensor-core launch template
+  size_t o_lo = 0;                 // lo_off table (128 int64) in the blob
+  size_t o_holo = 0, o_hohi = 0;   // two-level row-block base tables
+  bool has_ho = false;
+  size_t o_tcseg = 0, o_tckraw = 0; // tensor-core raw-ring tables
+  size_t o_folo = 0, o_fohi = 0;   // two-level tile base tables (SIMT tiles)
+  bool has_fo = false;
 };
 
 namespace {
@@ -387,7 +408,7 @@ int build_pair_plan(tnc_pair_plan& P, int dtype, int a_rank, const int64_t* a_di
   bool identity_a = true;
   for (size_t i = 0; i < fa.size(); ++i) identity_a = identity_a && perm[i] == (int)i;
   const int64_t tile_max = dtype == TNC_C64 ? 4096 : 2048;   // one ring stage: 32 KiB
-  std::vector<int64_t> segoff;
+  std::vector<int64_t> segoff, folo, fohi;
   std::vector<int32_t> rowoff, koff;
   P.kind = TNC_K_GENERIC;
   if (identity_a && K * N <= 4096 && (N <= 32 || K <= 16) && a_rank > 0) {
@@ -415,6 +436,27 @@ int build_pair_plan(tnc_pair_plan& P, int dtype, int a_rank, const int64_t* a_di
       for (size_t j = 0; j < of.size(); ++j) { pt.fo_dim[j] = a_dims[of[j]]; pt.fo_stride[j] = sa[of[j]]; pt.U *= a_dims[of[j]]; }
       pt.conj_b = conj_b ? 1 : 0;
       pt.Kout = kout; pt.Lseg = lseg; pt.R = R; pt.K = K; pt.N = N;
+      {
+        const int nfo = pt.nfo;
+        int split = nfo;
+        int64_t plo = 1;
+        while (split > 0 && plo * pt.fo_dim[split - 1] <= 4096) { plo *= pt.fo_dim[split - 1]; --split; }
+        int64_t phi = 1;
+        for (int i = 0; i < split; ++i) phi *= pt.fo_dim[i];
+        if (nfo > 1 && phi <= (1 << 20)) {
+          auto fill = [&](int from, int to, int64_t count, std::vector<int64_t>& outv) {
+            outv.resize(count);
+            for (int64_t m = 0; m < count; ++m) {
+              int64_t r = m, off = 0;
+              for (int i = to - 1; i >= from; --i) { off += (r % pt.fo_dim[i]) * pt.fo_stride[i]; r /= pt.fo_dim[i]; }
+              outv[m] = off;
+            }
+          };
+          fill(split, nfo, plo, folo);
+          fill(0, split, phi, fohi);
+          pt.f_plo = plo;
+        }
+      }
       segoff.resize(kout);
       std::vector<int64_t> segw(a_rank, 0);
       { int64_t w = 1; for (int j = (int)os.size() - 1; j >= 0; --j) { segw[os[j]] = w; w *= a_dims[os[j]]; } }
@@ -448,6 +490,94 @@ int build_pair_plan(tnc_pair_plan& P, int dtype, int a_rank, const int64_t* a_di
       P.kind = TNC_K_SKINNY;
     }
   }
+  // tensor-core envelope: complex64, identity result layout, a 128-row block
+  // made of the innermost free legs
+  std::vector<int64_t> looff, holo, hohi, tcseg;
+  std::vector<int32_t> tckraw;
+  {
+    bool identity = true;
+    for (int i = 0; i < nout; ++i) identity = identity && perm[i] == i;
+    if (dtype == TNC_C64 && identity && tnc::tc_shape_ok(K, N, d.M)) {
+      std::vector<char> shared(a_rank, 0);
+      for (int i = 0; i < npairs; ++i) shared[pair_a[i]] = 1;
+      int64_t prod_in = 1;
+      int t = a_rank;
+      std::vector<int> inner;
+      while (t > 0 && prod_in < 128) {
+        --t;
+        if (!shared[t]) { inner.insert(inner.begin(), t); prod_in *= a_dims[t]; }
+      }
+      if (prod_in == 128) {
+        tnc::TcDesc& c = P.tc;
+        memset(&c, 0, sizeof c);
+        c.M = d.M; c.K = K; c.N = N;
+        c.conj_b = conj_b ? 1 : 0;
+        c.slices_per_b = 1;
+        int nho = 0;
+        for (int i = 0; i < t; ++i) if (!shared[i]) { c.ho_dim[nho] = a_dims[i]; c.ho_stride[nho] = sa[i]; ++nho; }
+        c.nho = nho;
+        // two-level row-block base tables over the outer free legs
+        {
+          int split = nho;                 // legs [split, nho) form the low group
+          int64_t plo = 1;
+          while (split > 0 && plo * c.ho_dim[split - 1] <= 4096) { plo *= c.ho_dim[split - 1]; --split; }
+          int64_t phi = 1;
+          for (int i = 0; i < split; ++i) phi *= c.ho_dim[i];
+          if (phi <= (1 << 20) && plo * phi < (1LL << 31)) {
+            auto fill = [&](int from, int to, int64_t count, std::vector<int64_t>& outv) {
+              outv.resize(count);
+              for (int64_t m = 0; m < count; ++m) {
+                int64_t r = m, off = 0;
+                for (int i = to - 1; i >= from; --i) { off += (r % c.ho_dim[i]) * c.ho_stride[i]; r /= c.ho_dim[i]; }
+                outv[m] = off;
+              }
+            };
+            fill(split, nho, plo, holo);
+            fill(0, split, phi, hohi);
+            c.p_lo = plo;
+          }
+        }
+        // raw-ring geometry: span = legs [t, a_rank) (the 7 row legs + inner shared legs)
+        {
+          int64_t lseg = 1;
+          for (int i = t; i < a_rank; ++i) lseg *= a_dims[i];
+          std::vector<int> outer_sh;
+          for (int i = 0; i < t; ++i) if (shared[i]) outer_sh.push_back(i);
+          int64_t kout = 1;
+          for (int i : outer_sh) kout *= a_dims[i];
+          std::vector<int64_t> segw(a_rank, 0);
+          { int64_t w = 1; for (int j = (int)outer_sh.size() - 1; j >= 0; --j) { segw[outer_sh[j]] = w; w *= a_dims[outer_sh[j]]; } }
+          tcseg.resize(kout);
+          for (int64_t j = 0; j < kout; ++j) {
+            int64_t r = j, off = 0;
+            for (int q = (int)outer_sh.size() - 1; q >= 0; --q) { off += (r % a_dims[outer_sh[q]]) * sa[outer_sh[q]]; r /= a_dims[outer_sh[q]]; }
+            tcseg[j] = off;
+          }
+          tckraw.resize(K);
+          for (int64_t k0 = 0; k0 < K; ++k0) {
+            int64_t r = k0, seg = 0, inner = 0;
+            for (int i = npairs - 1; i >= 0; --i) {
+              const int ax = pair_a[i];
+              const int64_t dm = a_dims[ax], dg = r % dm;
+              r /= dm;
+              if (ax < t) seg += dg * segw[ax]; else inner += dg * sa[ax];
+            }
+            tckraw[k0] = (int32_t)(seg * lseg + inner);
+          }
+          c.Kout = kout;
+          c.Lseg = lseg;
+          c.raw_ok = (kout * lseg == 128 * K && (lseg * 8) % 16 == 0) ? 1 : 0;
+        }
+        looff.resize(128);
+        for (int r0 = 0; r0 < 128; ++r0) {
+          int64_t r = r0, off = 0;
+          for (int q = (int)inner.size() - 1; q >= 0; --q) { off += (r % a_dims[inner[q]]) * sa[inner[q]]; r /= a_dims[inner[q]]; }
+          looff[r0] = off;
+        }
+        P.tc_ok = true;
+      }
+    }
+  }
   // blob layout (8-byte aligned sections)
   size_t o = 0;
   P.o_ak = o; o += K * 8;
@@ -458,12 +588,30 @@ int build_pair_plan(tnc_pair_plan& P, int dtype, int a_rank, const int64_t* a_di
   P.o_row = o; o += rowoff.size() * 4;
   o = (o + 7) & ~(size_t)7;
   P.o_k = o; o += koff.size() * 4;
+  o = (o + 7) & ~(size_t)7;
+  P.o_lo = o; o += looff.size() * 8;
+  P.o_holo = o; o += holo.size() * 8;
+  P.o_hohi = o; o += hohi.size() * 8;
+  P.has_ho = !holo.empty();
+  P.o_tcseg = o; o += tcseg.size() * 8;
+  P.o_tckraw = o; o += tckraw.size() * 4;
+  o = (o + 7) & ~(size_t)7;
+  P.o_folo = o; o += folo.size() * 8;
+  P.o_fohi = o; o += fohi.size() * 8;
+  P.has_fo = !folo.empty();
   P.blob.assign(o + 8, 0);
   memcpy(P.blob.data() + P.o_ak, tab.data(), 2 * K * 8);                    // a_koff, b_koff
   memcpy(P.blob.data() + P.o_bn, tab.data() + 2 * K, N * 8 * 2);             // b_noff, c_noff
   if (!segoff.empty()) memcpy(P.blob.data() + P.o_seg, segoff.data(), segoff.size() * 8);
   if (!rowoff.empty()) memcpy(P.blob.data() + P.o_row, rowoff.data(), rowoff.size() * 4);
   if (!koff.empty()) memcpy(P.blob.data() + P.o_k, koff.data(), koff.size() * 4);
+  if (!looff.empty()) memcpy(P.blob.data() + P.o_lo, looff.data(), looff.size() * 8);
+  if (!holo.empty()) memcpy(P.blob.data() + P.o_holo, holo.data(), holo.size() * 8);
+  if (!hohi.empty()) memcpy(P.blob.data() + P.o_hohi, hohi.data(), hohi.size() * 8);
+  if (!tcseg.empty()) memcpy(P.blob.data() + P.o_tcseg, tcseg.data(), tcseg.size() * 8);
+  if (!tckraw.empty()) memcpy(P.blob.data() + P.o_tckraw, tckraw.data(), tckraw.size() * 4);
+  if (!folo.empty()) memcpy(P.blob.data() + P.o_folo, folo.data(), folo.size() * 8);
+  if (!fohi.empty()) memcpy(P.blob.data() + P.o_fohi, fohi.data(), fohi.size() * 8);
   return TNC_OK;
 }
 
@@ -478,11 +626,32 @@ void bind_tables(tnc_pair_plan& P, void* dev) {
   P.pt.segoff = reinterpret_cast<const int64_t*>(w + P.o_seg);
   P.pt.rowoff = reinterpret_cast<const int32_t*>(w + P.o_row);
   P.pt.koff = reinterpret_cast<const int32_t*>(w + P.o_k);
+  P.tc.akoff = P.d.a_koff;
+  P.tc.lo_off = reinterpret_cast<const int64_t*>(w + P.o_lo);
+  P.tc.segoff = reinterpret_cast<const int64_t*>(w + P.o_tcseg);
+  P.tc.kraw = reinterpret_cast<const int32_t*>(w + P.o_tckraw);
+  P.pt.fo_lo = P.has_fo ? reinterpret_cast<const int64_t*>(w + P.o_folo) : nullptr;
+  P.pt.fo_hi = P.has_fo ? reinterpret_cast<const int64_t*>(w + P.o_fohi) : nullptr;
+  P.tc.ho_lo = P.has_ho ? reinterpret_cast<const int64_t*>(w + P.o_holo) : nullptr;
+  P.tc.ho_hi = P.has_ho ? reinterpret_cast<const int64_t*>(w + P.o_hohi) : nullptr;
+  P.tc.b_koff = P.d.b_koff;
+  P.tc.b_noff = P.d.b_noff;
 }
 
 int execute_pair_plan(const tnc_pair_plan& P, int64_t batch, const void* a, int64_t a_zstride, const void* b,
                       int64_t b_zstride, void* out, int64_t out_zstride, cudaStream_t s) {
   if (batch <= 0) return TNC_OK;
+  if (P.tc_ok && tc_enabled() && P.tc.K * P.tc.N >= 256) {
+    tnc::TcDesc c = P.tc;
+    c.a = reinterpret_cast<const float2*>(a);
+    c.a_zstride = a_zstride;
+    c.site.ptr = b;
+    c.site.zstride = b_zstride;
+    c.out = reinterpret_cast<float2*>(out);
+    c.out_zstride = out_zstride;
+    if (tnc::launch_tc(c, batch, s) != 0) return check_launch("contract_pair[tc]");
+    return TNC_OK;
+  }
   if (P.kind == TNC_K_SKINNY) {
     tnc::PairTile pt = P.pt;
     pt.a_zstride = a_zstride; pt.b_zstride = b_zstride; pt.out_zstride = out_zstride;
@@ -504,10 +673,13 @@ extern "C" {
 
 size_t tnc_contract_pair_workspace(int a_rank, const int64_t* a_dims, int b_rank, const int64_t* b_dims,
                                    int npairs, const int32_t* pair_a, const int32_t* pair_b) {
-  std::vector<int> fa, fb;
-  int64_t K, N;
-  pair_layout(a_rank, a_dims, b_rank, b_dims, npairs, pair_a, pair_b, fa, fb, K, N);
-  return (size_t)(2 * K + 2 * N) * 8 + (size_t)K * 8 + 8192 * 4 + (size_t)K * 4 + 64;
+  tnc_pair_plan P;
+  if (build_pair_plan(P, TNC_C64, a_rank, a_dims, b_rank, b_dims, npairs, pair_a, pair_b, nullptr, 0) != TNC_OK)
+    return 0;
+  tnc_pair_plan Q;
+  if (build_pair_plan(Q, TNC_C128, a_rank, a_dims, b_rank, b_dims, npairs, pair_a, pair_b, nullptr, 0) != TNC_OK)
+    return 0;
+  return std::max(P.blob.size(), Q.blob.size()) + 256;
 }
 
 int tnc_contract_pair(int dtype, int64_t batch,
@@ -560,7 +732,11 @@ int tnc_pair_plan_execute(const tnc_pair_plan* plan, int64_t batch, const void* 
   return execute_pair_plan(*plan, batch, a, a_zstride, b, b_zstride, out, out_zstride, (cudaStream_t)stream);
 }
 
-int tnc_pair_plan_kernel(const tnc_pair_plan* plan) { return plan ? plan->kind : TNC_E_INVALID; }
+int tnc_pair_plan_kernel(const tnc_pair_plan* plan) {
+  if (!plan) return TNC_E_INVALID;
+  if (plan->tc_ok && tc_enabled() && plan->tc.K * plan->tc.N >= 256) return TNC_K_TC;
+  return plan->kind;
+}
 
 void tnc_pair_plan_destroy(tnc_pair_plan* plan) {
   if (!plan) return;

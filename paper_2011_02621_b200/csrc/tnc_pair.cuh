@@ -24,6 +24,9 @@ struct PairTile {
   const int64_t* b_noff;       // [N]
   int32_t vec16;               // segment base offsets and Lseg allow 16-byte copies
   int32_t pipe;                // use the pipelined persistent kernel when alignment allows
+  const int64_t* fo_lo;        // optional two-level tile base tables:
+  const int64_t* fo_hi;        //   base(u) = fo_hi[u / f_plo] + fo_lo[u % f_plo]
+  int64_t f_plo;
 };
 
 template <typename C>
@@ -59,6 +62,10 @@ __device__ __forceinline__ void stage_site(const PairTile& p, const C* __restric
 
 __device__ __forceinline__ int64_t tile_base(const PairTile& p, int64_t z, int64_t u) {
   int64_t base = z * p.a_zstride;
+  if (p.fo_lo) {
+    const int64_t q = u / p.f_plo;
+    return base + __ldg(p.fo_hi + q) + __ldg(p.fo_lo + (u - q * p.f_plo));
+  }
   for (int j = p.nfo - 1; j >= 0; --j) {
     const int64_t q = u / p.fo_dim[j];
     base += (u - q * p.fo_dim[j]) * p.fo_stride[j];

@@ -1,10 +1,592 @@
-// Tensor-core contraction path (tcgen05 3xTF32 for complex64, DMMA for
-// complex128).  try_tc returns 1 when it launched, 0 when the step is outside
-// its envelope.
+// Tensor-core contraction step for complex64: tcgen05.mma kind::tf32 with a
+// 3xTF32 split (hi*hi + hi*lo + lo*hi, fp32 accumulation in TMEM) so the
+// result keeps ~fp32 accuracy (north-star tolerance 1e-4 for complex64).
+//
+// Complex -> real embedding: an accumulator row [a_0 .. a_{K-1}] (interleaved
+// re/im) is the real row A' = [Re a_0, Im a_0, ...] of length 2K; the site block
+// S[K][N] becomes B' (2K x 2N) with B'[(k,re),(n,re)] = Re s, B'[(k,im),(n,re)] =
+// -Im s, B'[(k,re),(n,im)] = Im s, B'[(k,im),(n,im)] = Re s, so D = A' B' is the
+// interleaved complex result row.  A persistent CTA (one wave, <= #SMs) owns
+// a contiguous range of 128-row tiles over (batch element z, row block); the
+// MMA warp rebuilds B' in place when its tiles cross into a new z.
+//
+// Warp roles (416 threads): warps 0-7 convert accumulator chunks (global ->
+// tf32 hi/lo -> canonical K-major smem), warps 8-11 drain TMEM (epilogue),
+// warp 12 issues the MMAs.  Pipelines: A-chunk ring (2 stages, mbarriers),
+// TMEM accumulators (2 stages).
 #pragma once
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
 #include "tnc_common.cuh"
 
 namespace tnc {
+
+struct TcDesc {
+  int64_t M, K, N;                 // rows per batch element (multiple of 128)
+  int64_t tiles_per_z, per_cta, Z;
+  const float2* a;
+  int64_t a_zstride;
+  int32_t nho;                     // outer free legs above the 128-row block
+  int32_t conj_b;
+  int64_t ho_dim[TNC_MAX_LEGS], ho_stride[TNC_MAX_LEGS];
+  const int64_t* lo_off;           // [128] accumulator offset of row r inside a block
+  const int64_t* akoff;            // [K]
+  tnc_site site;
+  int64_t slices_per_b, s0;
+  const int64_t* b_koff;           // [K]
+  const int64_t* b_noff;           // [N]
+  float2* out;
+  int64_t out_zstride;             // out rows are contiguous: out + z*zs + g*N + n
+  int32_t rows_contig;             // lo_off[r] = r*K and akoff[k] = k (tables unused)
+  int32_t nstages;                 // A-chunk ring depth (host: as many as fit)
+  int32_t dbg;                     // experiment flags (0 in production): 1 no stores, 2 no loads, 4 no MMA
+  int32_t _pad2;
+  unsigned long long* trace;       // dbg & 128: per-tile globaltimer stamps of CTA 0
+  // raw-ring mode: each tile's 128 x K accumulator block is staged by cp.async.bulk
+  // as Kout contiguous segments of Lseg elements; element (r, k) sits at
+  // lo_off[r] + kraw[k] inside the staged tile
+  int32_t raw_stages;              // 0: converters gather from global directly
+  int32_t raw_ok;                  // host: layout admits the raw ring
+  int64_t Kout, Lseg;
+  const int64_t* segoff;           // [Kout] segment offsets from the tile base
+  const int32_t* kraw;             // [K]
+  const int64_t* ho_lo;            // optional two-level row-block base tables:
+  const int64_t* ho_hi;            //   base(m) = ho_hi[m / p_lo] + ho_lo[m % p_lo]
+  int64_t p_lo;
+};
+
+constexpr int TC_CONV_WARPS = 8;
+constexpr int TC_EPI_WARP0 = 8;
+constexpr int TC_MMA_WARP = 12;
+constexpr int TC_PROD_WARP = 13;         // raw-ring producer (cp.async.bulk)
+constexpr int TC_THREADS = 14 * 32;
+constexpr int TC_MAX_STAGES = 8;
+constexpr int TC_MAX_TILES = 2048;      // tiles per CTA (one wave; smem base table)
+
+__device__ __forceinline__ uint32_t tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+// hi = tf32(x), lo = tf32(x - hi)
+__device__ __forceinline__ void split3(float x, float& hi, float& lo) {
+  const uint32_t h = tf32_rna(x);
+  hi = __uint_as_float(h);
+  lo = __uint_as_float(tf32_rna(x - hi));
+}
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;          // descriptor version (sm_100)
+  return d;                        // base_offset 0, lbo_mode 0, SWIZZLE_NONE
+}
+
+__device__ __forceinline__ uint32_t tf32_idesc(int n_real) {
+  return (1u << 4)                 // D f32
+       | (2u << 7) | (2u << 10)    // A, B tf32
+       | ((uint32_t)(n_real >> 3) << 17)
+       | ((uint32_t)(128 >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+      ::"r"(d_tmem), "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+               ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TC_TRACE(slot, t) do { if ((p.dbg & 128) && blockIdx.x == 0 && (t) < 64 && (threadIdx.x & 31) == 0) p.trace[(slot) * 64 + (t)] = gtimer(); } while (0)
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// smem sizes (bytes) for a (K, N) problem
+__host__ __device__ inline int64_t tc_b_bytes(int64_t K, int64_t N) { return 2 * (2 * N) * (2 * K) * 4; }
+__host__ __device__ inline int64_t tc_kc(int64_t K) { return K >= 16 ? 16 : K; }
+__host__ __device__ inline int64_t tc_chunk_bytes(int64_t K) { return 128 * 2 * tc_kc(K) * 4; }  // one of hi/lo
+constexpr int TC_EPI_PITCH = 144;        // bytes per staged row (128 + 16 pad: conflict-free)
+__host__ __device__ inline int64_t tc_raw_bytes(int64_t K) { return 128 * K * 8; }
+__host__ __device__ inline int64_t tc_fixed_bytes(int64_t K, int64_t N, int64_t per, int64_t rs) {
+  return 1024 + tc_b_bytes(K, N) + K * 8 + K * 4 + 128 * 8 + 6 * TC_MAX_STAGES * 8 + 128 + per * 8
+         + 4 * 32 * TC_EPI_PITCH + 16 + rs * tc_raw_bytes(K);
+}
+__host__ __device__ inline int64_t tc_stages_for(int64_t K, int64_t N, int64_t per, int64_t rs = 0) {
+  const int64_t avail = 227 * 1024 - tc_fixed_bytes(K, N, per, rs);
+  if (avail <= 0) return 0;
+  int64_t st = avail / (2 * tc_chunk_bytes(K));
+  return st > TC_MAX_STAGES ? TC_MAX_STAGES : st;
+}
+__host__ __device__ inline int64_t tc_smem_bytes(int64_t K, int64_t N, int64_t per, int64_t rs = 0) {
+  return tc_fixed_bytes(K, N, per, rs) + tc_stages_for(K, N, per, rs) * 2 * tc_chunk_bytes(K);
+}
+
+// B' (hi, lo) for batch element z, written by threads [tid0, tid0 + nthr)
+__device__ __forceinline__ void build_b(const TcDesc& p, int64_t z, float* Bhi, float* Blo, int tid, int nthr) {
+  const int K = (int)p.K, N = (int)p.N;
+  const uint32_t SBO_B = ((2 * K) / 4) * 128;
+  const float2* S = reinterpret_cast<const float2*>(p.site.ptr) + site_offset(p.site, z, p.slices_per_b, p.s0);
+  for (int e = tid; e < K * N; e += nthr) {
+    const int k = e / N, n = e - (e / N) * N;
+    float2 sv = __ldg(S + p.b_koff[k] + p.b_noff[n]);
+    if (p.conj_b) sv.y = -sv.y;
+    // rows n' = 2n (re out), 2n+1 (im out); cols k' = 2k (re in), 2k+1 (im in)
+    const float vals[4] = {sv.x, -sv.y, sv.y, sv.x};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int nr = 2 * n + (q >> 1), kr = 2 * k + (q & 1);
+      const uint32_t off = (nr & 7) * 16 + (nr >> 3) * SBO_B + (kr >> 2) * 128 + (kr & 3) * 4;
+      float h, l;
+      split3(vals[q], h, l);
+      *reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(Bhi) + off) = h;
+      *reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(Blo) + off) = l;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+k_tc_c64(const __grid_constant__ TcDesc p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int K = (int)p.K, N = (int)p.N;
+  const int Kr = 2 * K, Nr = 2 * N;
+  const int KC = (int)tc_kc(p.K), nchunk = K / KC;
+  const int units = 2 * KC / 4;                  // 16-byte units per row of a chunk
+  const uint32_t SBO_A = units * 128, SBO_B = (Kr / 4) * 128;
+  // carve shared memory (1024-aligned base)
+  unsigned char* base = smem_raw;
+  float* Bhi = reinterpret_cast<float*>(base);
+  float* Blo = Bhi + (size_t)Nr * Kr;
+  unsigned char* ring = reinterpret_cast<unsigned char*>(Blo + (size_t)Nr * Kr);
+  const int64_t cbytes = tc_chunk_bytes(p.K);
+  const int NS = p.nstages;
+  const int RS = p.raw_stages;
+  unsigned char* rawring = ring + (size_t)NS * 2 * cbytes;       // [RS][128*K complex]
+  int64_t* akoff_s = reinterpret_cast<int64_t*>(rawring + (size_t)RS * tc_raw_bytes(p.K));
+  int64_t* looff_s = akoff_s + K;
+  int32_t* kraw_s = reinterpret_cast<int32_t*>(looff_s + 128);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(kraw_s + ((K + 1) & ~1));   // 6 x TC_MAX_STAGES barriers
+  uint64_t* full = bar;                        // [NS] converters -> MMA
+  uint64_t* empty = bar + TC_MAX_STAGES;       // [NS] MMA commit -> converters
+  uint64_t* tfull = bar + 2 * TC_MAX_STAGES;   // [TS] MMA commit -> epilogue
+  uint64_t* tempty = tfull + TC_MAX_STAGES;    // [TS] epilogue -> MMA
+  uint64_t* rfull = tempty + TC_MAX_STAGES;    // [RS] bulk copy landed -> converters
+  uint64_t* rempty = rfull + TC_MAX_STAGES;    // [RS] converters done -> producer
+  uint64_t* bdone = rempty + TC_MAX_STAGES;    // MMA-warp-local: B' retire
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bdone + 1);
+  int64_t* tbase = reinterpret_cast<int64_t*>(bdone + 2);   // [per_cta] accumulator base of each tile
+  unsigned char* epi_stage = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(tbase + p.per_cta) + 15) & ~(uintptr_t)15);   // [4 warps][32 rows][144 B]
+  // TMEM accumulator ring: as many N'-column stages as fit in 512 columns (<= 8)
+  int TS = 512 / Nr;
+  if (TS > TC_MAX_STAGES) TS = TC_MAX_STAGES;
+
+  // global tile index g = z * tiles_per_z + m; this CTA owns [g0, g1)
+  const int64_t g0 = blockIdx.x * p.per_cta;
+  const int64_t g1 = min(g0 + p.per_cta, p.Z * p.tiles_per_z);
+  const int ntiles = (int)(g1 - g0);
+  const int64_t z0 = g0 / p.tiles_per_z;
+
+  // ---- setup: barriers, TMEM, tables, B' (hi/lo) ----
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], TC_CONV_WARPS);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < TS; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 4);
+    }
+    mbar_init(bdone, 1);
+    for (int s = 0; s < RS; ++s) {
+      mbar_init(&rfull[s], 1);
+      mbar_init(&rempty[s], TC_CONV_WARPS);
+    }
+    mbar_fence_init();
+  }
+  uint32_t ncols = 32;
+  while (ncols < (uint32_t)(TS * Nr)) ncols <<= 1;
+  if (warp == TC_EPI_WARP0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(smem_u32(tmem_slot)), "r"(ncols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  for (int k = threadIdx.x; k < K; k += blockDim.x) akoff_s[k] = p.rows_contig ? k : p.akoff[k];
+  for (int r = threadIdx.x; r < 128; r += blockDim.x) looff_s[r] = p.rows_contig ? (int64_t)r * K : p.lo_off[r];
+  for (int k = threadIdx.x; k < K && RS > 0; k += blockDim.x) kraw_s[k] = p.rows_contig ? k : p.kraw[k];
+  if (ntiles > 0) build_b(p, z0, Bhi, Blo, threadIdx.x, blockDim.x);
+  for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
+    const int64_t g = g0 + t;
+    const int64_t zt = g / p.tiles_per_z;
+    int64_t mb = g - zt * p.tiles_per_z, hb = zt * p.a_zstride;
+    if (p.ho_lo) {
+      const int64_t q = mb / p.p_lo;
+      hb += __ldg(p.ho_hi + q) + __ldg(p.ho_lo + (mb - q * p.p_lo));
+    } else {
+      for (int j = p.nho - 1; j >= 0; --j) {
+        const int64_t q = mb / p.ho_dim[j];
+        hb += (mb - q * p.ho_dim[j]) * p.ho_stride[j];
+        mb = q;
+      }
+    }
+    tbase[t] = hb;
+  }
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < TC_CONV_WARPS) {
+    // ---------------- converters: row r = tid % 128, half h = tid / 128 ----------------
+    // Loads run TC_PF chunks ahead of the smem stores (register ring, static
+    // indexing via a 3-way unrolled loop) to keep ~48 KiB in flight per SM.
+    const int r = threadIdx.x & 127, h = threadIdx.x >> 7;
+    const int kh = KC / 2;                 // complex per thread per chunk (KC even)
+    const float2* A = p.a + looff_s[r];
+    const int total = ntiles * nchunk;
+    auto row_base = [&](int t) -> const float2* { return A + tbase[t]; };
+    auto load = [&](float2 (&v)[8], int it) {
+      if (it >= total || RS > 0) return;
+      const int t = it / nchunk, c = it - t * nchunk;
+      const float2* Ar = row_base(t);
+      const int64_t* ko = akoff_s + c * KC + h * kh;
+      if (p.dbg & 2) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = make_float2(1.f, 0.f);
+        return;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q < kh) v[q] = __ldg(Ar + ko[q]);
+    };
+    auto store = [&](const float2 (&vin)[8], int it) {
+      const int stage = it % NS;
+      const uint32_t ph = (it / NS) & 1;
+      float2 v[8];
+      const int tt = it / nchunk, cc = it - tt * nchunk;
+      if (RS > 0) {
+        // gather this thread's chunk values out of the staged raw tile
+        const int rs = tt % RS;
+        if (cc == 0) mbar_wait(&rfull[rs], (uint32_t)((tt / RS) & 1));
+        const float2* raw = reinterpret_cast<const float2*>(rawring + (size_t)rs * tc_raw_bytes(p.K)) + looff_s[r];
+        const int32_t* kr = kraw_s + cc * KC + h * kh;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q < kh) v[q] = raw[kr[q]];
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = vin[q];
+      }
+      if (warp == 0) TC_TRACE(0, it);
+      mbar_wait(&empty[stage], ph ^ 1);
+      if (warp == 0) TC_TRACE(1, it);
+      unsigned char* chi = ring + (size_t)stage * 2 * cbytes;
+      unsigned char* clo = chi + cbytes;
+      const uint32_t rbase = (r & 7) * 16 + (r >> 3) * SBO_A;
+#pragma unroll
+      for (int q = 0; q < 8; q += 2) {
+        if (q < kh) {
+          const int kk = h * kh + q;
+          const uint32_t off = rbase + (uint32_t)(kk >> 1) * 128;
+          float4 hi, lo;
+          split3(v[q].x, hi.x, lo.x);
+          split3(v[q].y, hi.y, lo.y);
+          split3(v[q + 1].x, hi.z, lo.z);
+          split3(v[q + 1].y, hi.w, lo.w);
+          if (!(p.dbg & 16)) {
+            *reinterpret_cast<float4*>(chi + off) = hi;
+            *reinterpret_cast<float4*>(clo + off) = lo;
+          }
+        }
+      }
+      if (!(p.dbg & 8)) fence_proxy_async();
+      mbar_arrive_warp(&full[stage]);
+      if (RS > 0 && cc == nchunk - 1) mbar_arrive_warp(&rempty[tt % RS]);
+      if (warp == 0) TC_TRACE(2, it);
+    };
+    float2 v0[8], v1[8], v2[8];
+    load(v0, 0);
+    load(v1, 1);
+    for (int it = 0; it < total; it += 3) {
+      load(v2, it + 2);
+      store(v0, it);
+      if (it + 1 >= total) break;
+      load(v0, it + 3);
+      store(v1, it + 1);
+      if (it + 2 >= total) break;
+      load(v1, it + 4);
+      store(v2, it + 2);
+    }
+  } else if (warp < TC_MMA_WARP) {
+    // ---------------- epilogue: TMEM -> registers -> global ----------------
+    const int q = warp - TC_EPI_WARP0;     // lane quarter
+    const int r = q * 32 + lane;           // tile row
+    for (int t = 0; t < ntiles; ++t) {
+      const int acc = t % TS;
+      const uint32_t ph = (t / TS) & 1;
+      if (q == 0) TC_TRACE(3, t);
+      mbar_wait(&tfull[acc], ph);
+      if (q == 0) TC_TRACE(4, t);
+      tc_fence_after();
+      const int64_t gt = g0 + t;
+      const int64_t zt = gt / p.tiles_per_z;
+      const int64_t grow = (gt - zt * p.tiles_per_z) * 128 + r;
+      float2* otile = p.out + zt * p.out_zstride + (grow - lane) * N;   // this warp's 32 rows
+      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * Nr);
+      unsigned char* stg = epi_stage + q * 32 * TC_EPI_PITCH;
+      for (int c0 = 0; c0 < Nr; c0 += 32) {
+        const int cols = (c0 + 32 <= Nr) ? 32 : 16;       // real columns in this chunk
+        uint32_t v[32];
+        if (cols == 32) {
+          tmem_ld32(taddr + c0, v);
+        } else {
+          uint32_t w16[16];
+          tmem_ld16(taddr + c0, w16);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = w16[j];
+        }
+        tmem_wait_ld();
+        // registers -> padded staging rows (lane = row), conflict-free 16-byte stores
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (4 * j < cols)
+            *reinterpret_cast<uint4*>(stg + lane * TC_EPI_PITCH + j * 16) =
+                make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        __syncwarp();
+        // staging -> global: 8 (or 4) lanes per row, whole 128-byte lines per instruction
+        const int per_row = cols / 4;                       // 16-byte pieces per row
+        if (!(p.dbg & 1)) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int idx = i * 32 + lane;
+            const int row = idx / per_row, piece = idx - row * per_row;
+            if (row < 32) {
+              const uint4 val = *reinterpret_cast<const uint4*>(stg + row * TC_EPI_PITCH + piece * 16);
+              *reinterpret_cast<uint4*>(reinterpret_cast<unsigned char*>(otile + (int64_t)row * N + c0 / 2) + piece * 16) = val;
+            }
+          }
+        }
+        __syncwarp();
+      }
+      tc_fence_before();
+      mbar_arrive_warp(&tempty[acc]);
+      if (q == 0) TC_TRACE(5, t);
+    }
+  } else if (warp == TC_MMA_WARP) {
+    // ---------------- MMA issuer ----------------
+    const uint32_t idesc = tf32_idesc(Nr);
+    const uint32_t bhi = smem_u32(Bhi), blo = smem_u32(Blo);
+    int it = 0;
+    int64_t cur_z = z0;
+    uint32_t bdone_phase = 0;
+    for (int t = 0; t < ntiles; ++t) {
+      const int64_t zt = (g0 + t) / p.tiles_per_z;
+      if (zt != cur_z) {
+        // all MMAs reading the old B' must retire before it is rewritten
+        if (lane == 0) umma_commit(bdone);
+        __syncwarp();
+        mbar_wait(bdone, bdone_phase);
+        bdone_phase ^= 1;
+        tc_fence_after();
+        build_b(p, zt, Bhi, Blo, lane, 32);
+        fence_proxy_async();
+        __syncwarp();
+        tc_fence_before();
+        cur_z = zt;
+      }
+      const int acc = t % TS;
+      const uint32_t aph = (t / TS) & 1;
+      TC_TRACE(6, t);
+      mbar_wait(&tempty[acc], aph ^ 1);
+      TC_TRACE(7, t);
+      tc_fence_after();
+      const uint32_t d = tmem + (uint32_t)(acc * Nr);
+      for (int c = 0; c < nchunk; ++c, ++it) {
+        const int stage = it % NS;
+        const uint32_t ph = (it / NS) & 1;
+        mbar_wait(&full[stage], ph);
+        TC_TRACE(8, it);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t ahi = smem_u32(ring + (size_t)stage * 2 * cbytes);
+          const uint64_t dah0 = umma_desc(ahi, 128, SBO_A);
+          const uint64_t dal0 = umma_desc(ahi + (uint32_t)cbytes, 128, SBO_A);
+          const uint64_t dbh0 = umma_desc(bhi + (uint32_t)(c * units) * 128, 128, SBO_B);
+          const uint64_t dbl0 = umma_desc(blo + (uint32_t)(c * units) * 128, 128, SBO_B);
+          for (int s = 0; s < KC / 4; ++s) {
+            const uint64_t step = (uint64_t)(s * 256) >> 4;     // start-address field, 16-byte units
+            const uint64_t dah = dah0 + step, dal = dal0 + step;
+            const uint64_t dbh = dbh0 + step, dbl = dbl0 + step;
+            const uint32_t first = (c == 0 && s == 0) ? 0u : 1u;
+            if (!(p.dbg & 4)) {
+              mma_tf32(d, dal, dbh, idesc, first);   // small terms first
+              mma_tf32(d, dah, dbl, idesc, 1u);
+              mma_tf32(d, dah, dbh, idesc, 1u);
+            }
+          }
+          umma_commit(&empty[stage]);
+          if (c == nchunk - 1) umma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        TC_TRACE(9, it);
+      }
+    }
+  }
+  else if (warp == TC_PROD_WARP && RS > 0 && lane == 0) {
+    // ---------------- raw-ring producer: cp.async.bulk of each tile's segments ----------------
+    const uint32_t seg_bytes = (uint32_t)(p.Lseg * 8);
+    for (int t = 0; t < ntiles; ++t) {
+      const int rs = t % RS;
+      mbar_wait(&rempty[rs], (uint32_t)(((t / RS) & 1) ^ 1));
+      unsigned char* dst = rawring + (size_t)rs * tc_raw_bytes(p.K);
+      const float2* src = p.a + tbase[t];
+      mbar_expect_tx(&rfull[rs], (uint32_t)(p.Kout * seg_bytes));
+      for (int64_t j = 0; j < p.Kout; ++j)
+        bulk_g2s(dst + j * seg_bytes, src + (p.segoff ? p.segoff[j] : 0), seg_bytes, &rfull[rs]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == TC_EPI_WARP0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols));
+  }
+}
+
+// envelope of the tensor-core kernel
+__host__ inline bool tc_shape_ok(int64_t K, int64_t N, int64_t M) {
+  if (K < 4 || K > 64 || (K % 4) != 0 || (K > 16 && (K % 16) != 0)) return false;
+  if (N < 8 || N > 128 || (N % 8) != 0 || (M % 128) != 0 || M <= 0) return false;
+  return tc_stages_for(K, N, 64) >= 2;
+}
+
+// returns 0 if launched, -1 on launch error
+__host__ inline int launch_tc(TcDesc p, int64_t Z, cudaStream_t s) {
+  static bool attr_done = false;
+  if (!attr_done) {
+    if (cudaFuncSetAttribute(k_tc_c64, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
+      return -1;
+    attr_done = true;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  p.tiles_per_z = p.M / 128;
+  {
+    const char* e = getenv("TNC_TC_DEBUG");
+    p.dbg = e ? atoi(e) : 0;
+  }
+  p.Z = Z;
+  const int64_t total = Z * p.tiles_per_z;
+  int64_t per = (total + sms - 1) / sms;
+  if (per < 1) per = 1;
+  while (per > 64 && tc_stages_for(p.K, p.N, per) < 3) per = (per + 1) / 2;   // keep >= 3 ring stages
+  p.per_cta = per;
+  // raw ring when alignment allows and at least 2 raw + 2 A stages fit
+  p.raw_stages = 0;
+  const bool aligned = (((uintptr_t)p.a) % 16 == 0) && ((p.a_zstride * 8) % 16 == 0);
+  if (p.raw_ok && aligned && !(p.dbg & 256)) {
+    for (int rs = 4; rs >= 2; --rs)
+      if (tc_stages_for(p.K, p.N, per, rs) >= 2) { p.raw_stages = rs; break; }
+  }
+  p.nstages = (int32_t)tc_stages_for(p.K, p.N, per, p.raw_stages);
+  if (p.nstages < 2) return -1;
+  const size_t smem = (size_t)tc_smem_bytes(p.K, p.N, per, p.raw_stages);
+  {
+    const char* st = getenv("TNC_TC_STAGES");
+    if (st && atoi(st) >= 2 && atoi(st) < p.nstages) p.nstages = atoi(st);
+  }
+  const int64_t grid = (total + per - 1) / per;     // one wave when per fits in smem
+  if (grid <= 0) return 0;
+  if (p.dbg & 128) {
+    cudaMalloc(&p.trace, 10 * 64 * sizeof(unsigned long long));
+    cudaMemset(p.trace, 0, 10 * 64 * sizeof(unsigned long long));
+  }
+  k_tc_c64<<<(unsigned)grid, TC_THREADS, smem, s>>>(p);
+  if (p.dbg & 128) {
+    unsigned long long h[640];
+    cudaStreamSynchronize(s);
+    cudaMemcpy(h, p.trace, sizeof h, cudaMemcpyDeviceToHost);
+    const unsigned long long t0 = h[0];
+    const char* names[10] = {"conv_pre_empty", "conv_got_empty", "conv_arrived", "epi_pre_tfull", "epi_got_tfull",
+                             "epi_arrived", "mma_pre_tempty", "mma_got_tempty", "mma_got_full", "mma_committed"};
+    for (int sl = 0; sl < 10; ++sl) {
+      printf("%-16s", names[sl]);
+      for (int t = 0; t < 24; ++t) printf(" %6lld", h[sl * 64 + t] ? (long long)(h[sl * 64 + t] - t0) : -1LL);
+      printf("\n");
+    }
+    cudaFree(p.trace);
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+// tnc_step entry: accumulator rows contiguous, result rows contiguous, complex64
 template <typename R>
-int try_tc(const tnc_step_desc&, cudaStream_t) { return 0; }
+int try_tc(const tnc_step_desc& d, cudaStream_t s) {
+  if constexpr (sizeof(R) != 4) {
+    return 0;
+  } else {
+    if (!d.a_rows_contig || !d.c_rows_contig) return 0;
+    if (!tc_shape_ok(d.K, d.N, d.M)) return 0;
+    if (d.kernel == TNC_K_AUTO && d.K * d.N < 256) return 0;   // SIMT is HBM-bound there
+    TcDesc p;
+    memset(&p, 0, sizeof p);
+    p.M = d.M; p.K = d.K; p.N = d.N;
+    p.a = reinterpret_cast<const float2*>(d.acc);
+    p.a_zstride = d.acc_zstride;
+    p.nho = 1;
+    p.ho_dim[0] = d.M / 128;
+    p.ho_stride[0] = 128 * d.K;
+    p.rows_contig = 1;
+    p.raw_ok = 1;
+    p.Kout = 1;
+    p.Lseg = 128 * d.K;
+    p.segoff = nullptr;
+    p.site = d.site;
+    p.slices_per_b = d.slices_per_b;
+    p.s0 = d.s0;
+    p.b_koff = d.b_koff;
+    p.b_noff = d.b_noff;
+    p.conj_b = d.conj_b;
+    p.out = reinterpret_cast<float2*>(d.out);
+    p.out_zstride = d.out_zstride;
+    return launch_tc(p, d.Z, s) == 0 ? 1 : -1;
+  }
+}
+
 }  // namespace tnc

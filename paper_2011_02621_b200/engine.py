@@ -554,7 +554,7 @@ class PairPlan:
     @property
     def kernel(self) -> str:
         k = self.L.tnc_pair_plan_kernel(self._h)
-        return {NV.K_SKINNY: "tiled-permute", NV.K_GENERIC: "generic"}.get(k, str(k))
+        return {NV.K_SKINNY: "tiled-permute", NV.K_GENERIC: "generic", NV.K_TC: "tcgen05-3xtf32"}.get(k, str(k))
 
     def __call__(self, a, b, out, batch: int, a_zstride: int, b_zstride: int, out_zstride: int, stream=None):
         import torch
