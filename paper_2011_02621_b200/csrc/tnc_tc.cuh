@@ -138,22 +138,45 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 // smem sizes (bytes) for a (K, N) problem
 __host__ __device__ inline int64_t tc_b_bytes(int64_t K, int64_t N) { return 2 * (2 * N) * (2 * K) * 4; }
 __host__ __device__ inline int64_t tc_kc(int64_t K) { return K >= 16 ? 16 : K; }
-__host__ __device__ inline int64_t tc_chunk_bytes(int64_t K) { return 128 * 2 * tc_kc(K) * 4; }  // one of hi/lo
 constexpr int TC_EPI_PITCH = 144;        // bytes per staged row (128 + 16 pad: conflict-free)
 __host__ __device__ inline int64_t tc_raw_bytes(int64_t K) { return 128 * K * 8; }
-__host__ __device__ inline int64_t tc_fixed_bytes(int64_t K, int64_t N, int64_t per, int64_t rs) {
+__host__ __device__ inline int64_t tc_smem_bytes(int64_t K, int64_t N, int64_t per, int64_t rs) {
   return 1024 + tc_b_bytes(K, N) + K * 8 + K * 4 + 128 * 8 + 6 * TC_MAX_STAGES * 8 + 128 + per * 8
          + 4 * 32 * TC_EPI_PITCH + 16 + rs * tc_raw_bytes(K);
 }
-__host__ __device__ inline int64_t tc_stages_for(int64_t K, int64_t N, int64_t per, int64_t rs = 0) {
-  const int64_t avail = 227 * 1024 - tc_fixed_bytes(K, N, per, rs);
-  if (avail <= 0) return 0;
-  int64_t st = avail / (2 * tc_chunk_bytes(K));
-  return st > TC_MAX_STAGES ? TC_MAX_STAGES : st;
+// TMEM plan: TS accumulators of Nr columns, AS A-chunk stages of 4*KC columns (hi + lo)
+__host__ __device__ inline void tc_tmem_plan(int64_t K, int64_t N, int& TS, int& AS) {
+  const int Nr = (int)(2 * N), kc = (int)tc_kc(K);
+  TS = 256 / Nr;
+  if (TS > TC_MAX_STAGES) TS = TC_MAX_STAGES;
+  if (TS < 2) TS = 2;
+  AS = (512 - TS * Nr) / (4 * kc);
+  if (AS > TC_MAX_STAGES) AS = TC_MAX_STAGES;
 }
-__host__ __device__ inline int64_t tc_smem_bytes(int64_t K, int64_t N, int64_t per, int64_t rs = 0) {
-  return tc_fixed_bytes(K, N, per, rs) + tc_stages_for(K, N, per, rs) * 2 * tc_chunk_bytes(K);
+
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}"
+      ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
+template <int NW>
+__device__ __forceinline__ void tmem_st(uint32_t taddr, const uint32_t (&v)[16]) {
+  if constexpr (NW == 16) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
+                 ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+                   "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]));
+  } else if constexpr (NW == 8) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                 ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]));
+  } else {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};"
+                 ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]));
+  }
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // B' (hi, lo) for batch element z, written by threads [tid0, tid0 + nthr)
 __device__ __forceinline__ void build_b(const TcDesc& p, int64_t z, float* Bhi, float* Blo, int tid, int nthr) {
@@ -178,30 +201,32 @@ __device__ __forceinline__ void build_b(const TcDesc& p, int64_t z, float* Bhi, 
   }
 }
 
+// KH = complex values per converter thread per chunk (KC / 2)
+template <int KH>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_tc_c64(const __grid_constant__ TcDesc p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
+  constexpr int KC = 2 * KH;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K = (int)p.K, N = (int)p.N;
   const int Kr = 2 * K, Nr = 2 * N;
-  const int KC = (int)tc_kc(p.K), nchunk = K / KC;
-  const int units = 2 * KC / 4;                  // 16-byte units per row of a chunk
-  const uint32_t SBO_A = units * 128, SBO_B = (Kr / 4) * 128;
-  // carve shared memory (1024-aligned base)
-  unsigned char* base = smem_raw;
-  float* Bhi = reinterpret_cast<float*>(base);
+  const int nchunk = K / KC;
+  const uint32_t SBO_B = (Kr / 4) * 128;
+  int TS, AS;
+  tc_tmem_plan(p.K, p.N, TS, AS);
+  const uint32_t A0 = (uint32_t)(TS * Nr);      // first A column
+  constexpr uint32_t ACOLS = 4 * KC;            // per A stage: hi (2KC) + lo (2KC)
+  // ---- shared memory carve-up ----
+  float* Bhi = reinterpret_cast<float*>(smem_raw);
   float* Blo = Bhi + (size_t)Nr * Kr;
-  unsigned char* ring = reinterpret_cast<unsigned char*>(Blo + (size_t)Nr * Kr);
-  const int64_t cbytes = tc_chunk_bytes(p.K);
-  const int NS = p.nstages;
+  unsigned char* rawring = reinterpret_cast<unsigned char*>(Blo + (size_t)Nr * Kr);   // [RS][128*K complex]
   const int RS = p.raw_stages;
-  unsigned char* rawring = ring + (size_t)NS * 2 * cbytes;       // [RS][128*K complex]
   int64_t* akoff_s = reinterpret_cast<int64_t*>(rawring + (size_t)RS * tc_raw_bytes(p.K));
   int64_t* looff_s = akoff_s + K;
   int32_t* kraw_s = reinterpret_cast<int32_t*>(looff_s + 128);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(kraw_s + ((K + 1) & ~1));   // 6 x TC_MAX_STAGES barriers
-  uint64_t* full = bar;                        // [NS] converters -> MMA
-  uint64_t* empty = bar + TC_MAX_STAGES;       // [NS] MMA commit -> converters
+  uint64_t* bar = reinterpret_cast<uint64_t*>(kraw_s + ((K + 1) & ~1));
+  uint64_t* full = bar;                        // [AS] converters -> MMA
+  uint64_t* empty = bar + TC_MAX_STAGES;       // [AS] MMA commit -> converters
   uint64_t* tfull = bar + 2 * TC_MAX_STAGES;   // [TS] MMA commit -> epilogue
   uint64_t* tempty = tfull + TC_MAX_STAGES;    // [TS] epilogue -> MMA
   uint64_t* rfull = tempty + TC_MAX_STAGES;    // [RS] bulk copy landed -> converters
@@ -211,9 +236,6 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
   int64_t* tbase = reinterpret_cast<int64_t*>(bdone + 2);   // [per_cta] accumulator base of each tile
   unsigned char* epi_stage = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(tbase + p.per_cta) + 15) & ~(uintptr_t)15);   // [4 warps][32 rows][144 B]
-  // TMEM accumulator ring: as many N'-column stages as fit in 512 columns (<= 8)
-  int TS = 512 / Nr;
-  if (TS > TC_MAX_STAGES) TS = TC_MAX_STAGES;
 
   // global tile index g = z * tiles_per_z + m; this CTA owns [g0, g1)
   const int64_t g0 = blockIdx.x * p.per_cta;
@@ -221,9 +243,9 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
   const int ntiles = (int)(g1 - g0);
   const int64_t z0 = g0 / p.tiles_per_z;
 
-  // ---- setup: barriers, TMEM, tables, B' (hi/lo) ----
+  // ---- setup ----
   if (threadIdx.x == 0) {
-    for (int s = 0; s < NS; ++s) {
+    for (int s = 0; s < AS; ++s) {
       mbar_init(&full[s], TC_CONV_WARPS);
       mbar_init(&empty[s], 1);
     }
@@ -231,18 +253,16 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 4);
     }
-    mbar_init(bdone, 1);
     for (int s = 0; s < RS; ++s) {
       mbar_init(&rfull[s], 1);
       mbar_init(&rempty[s], TC_CONV_WARPS);
     }
+    mbar_init(bdone, 1);
     mbar_fence_init();
   }
-  uint32_t ncols = 32;
-  while (ncols < (uint32_t)(TS * Nr)) ncols <<= 1;
   if (warp == TC_EPI_WARP0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                 ::"r"(smem_u32(tmem_slot)), "r"(ncols));
+                 ::"r"(smem_u32(tmem_slot)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   for (int k = threadIdx.x; k < K; k += blockDim.x) akoff_s[k] = p.rows_contig ? k : p.akoff[k];
@@ -272,74 +292,57 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
   const uint32_t tmem = *tmem_slot;
 
   if (warp < TC_CONV_WARPS) {
-    // ---------------- converters: row r = tid % 128, half h = tid / 128 ----------------
-    // Loads run TC_PF chunks ahead of the smem stores (register ring, static
-    // indexing via a 3-way unrolled loop) to keep ~48 KiB in flight per SM.
+    // ---------------- converters: row r = tid % 128 (TMEM lane), half h = tid / 128 ----------------
     const int r = threadIdx.x & 127, h = threadIdx.x >> 7;
-    const int kh = KC / 2;                 // complex per thread per chunk (KC even)
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     const float2* A = p.a + looff_s[r];
     const int total = ntiles * nchunk;
-    auto row_base = [&](int t) -> const float2* { return A + tbase[t]; };
-    auto load = [&](float2 (&v)[8], int it) {
+    auto load = [&](float2 (&v)[KH], int it) {
       if (it >= total || RS > 0) return;
       const int t = it / nchunk, c = it - t * nchunk;
-      const float2* Ar = row_base(t);
-      const int64_t* ko = akoff_s + c * KC + h * kh;
-      if (p.dbg & 2) {
+      const float2* Ar = A + tbase[t];
+      const int64_t* ko = akoff_s + c * KC + h * KH;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = make_float2(1.f, 0.f);
-        return;
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        if (q < kh) v[q] = __ldg(Ar + ko[q]);
+      for (int q = 0; q < KH; ++q) v[q] = __ldg(Ar + ko[q]);
     };
-    auto store = [&](const float2 (&vin)[8], int it) {
-      const int stage = it % NS;
-      const uint32_t ph = (it / NS) & 1;
-      float2 v[8];
+    auto store = [&](const float2 (&vin)[KH], int it) {
+      const int stage = it % AS;
+      const uint32_t ph = (it / AS) & 1;
       const int tt = it / nchunk, cc = it - tt * nchunk;
+      float2 v[KH];
       if (RS > 0) {
-        // gather this thread's chunk values out of the staged raw tile
         const int rs = tt % RS;
         if (cc == 0) mbar_wait(&rfull[rs], (uint32_t)((tt / RS) & 1));
         const float2* raw = reinterpret_cast<const float2*>(rawring + (size_t)rs * tc_raw_bytes(p.K)) + looff_s[r];
-        const int32_t* kr = kraw_s + cc * KC + h * kh;
+        const int32_t* kr = kraw_s + cc * KC + h * KH;
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (q < kh) v[q] = raw[kr[q]];
+        for (int q = 0; q < KH; ++q) v[q] = raw[kr[q]];
       } else {
 #pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = vin[q];
+        for (int q = 0; q < KH; ++q) v[q] = vin[q];
       }
-      if (warp == 0) TC_TRACE(0, it);
-      mbar_wait(&empty[stage], ph ^ 1);
-      if (warp == 0) TC_TRACE(1, it);
-      unsigned char* chi = ring + (size_t)stage * 2 * cbytes;
-      unsigned char* clo = chi + cbytes;
-      const uint32_t rbase = (r & 7) * 16 + (r >> 3) * SBO_A;
+      uint32_t hi[16], lo[16];
 #pragma unroll
-      for (int q = 0; q < 8; q += 2) {
-        if (q < kh) {
-          const int kk = h * kh + q;
-          const uint32_t off = rbase + (uint32_t)(kk >> 1) * 128;
-          float4 hi, lo;
-          split3(v[q].x, hi.x, lo.x);
-          split3(v[q].y, hi.y, lo.y);
-          split3(v[q + 1].x, hi.z, lo.z);
-          split3(v[q + 1].y, hi.w, lo.w);
-          if (!(p.dbg & 16)) {
-            *reinterpret_cast<float4*>(chi + off) = hi;
-            *reinterpret_cast<float4*>(clo + off) = lo;
-          }
-        }
+      for (int q = 0; q < KH; ++q) {
+        float a, b;
+        split3(v[q].x, a, b);
+        hi[2 * q] = __float_as_uint(a);
+        lo[2 * q] = __float_as_uint(b);
+        split3(v[q].y, a, b);
+        hi[2 * q + 1] = __float_as_uint(a);
+        lo[2 * q + 1] = __float_as_uint(b);
       }
-      if (!(p.dbg & 8)) fence_proxy_async();
+      if (RS > 0 && cc == nchunk - 1) mbar_arrive_warp(&rempty[tt % RS]);   // raw values are in registers
+      mbar_wait(&empty[stage], ph ^ 1);
+      tc_fence_after();
+      const uint32_t col = A0 + (uint32_t)stage * ACOLS + (uint32_t)(h * 2 * KH);
+      tmem_st<2 * KH>(tmem + lane_base + col, hi);
+      tmem_st<2 * KH>(tmem + lane_base + col + 2 * KC, lo);
+      tmem_wait_st();
+      tc_fence_before();
       mbar_arrive_warp(&full[stage]);
-      if (RS > 0 && cc == nchunk - 1) mbar_arrive_warp(&rempty[tt % RS]);
-      if (warp == 0) TC_TRACE(2, it);
     };
-    float2 v0[8], v1[8], v2[8];
+    float2 v0[KH], v1[KH], v2[KH];
     load(v0, 0);
     load(v1, 1);
     for (int it = 0; it < total; it += 3) {
@@ -353,24 +356,22 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
       store(v2, it + 2);
     }
   } else if (warp < TC_MMA_WARP) {
-    // ---------------- epilogue: TMEM -> registers -> global ----------------
+    // ---------------- epilogue: TMEM -> registers -> padded smem -> coalesced global ----------------
     const int q = warp - TC_EPI_WARP0;     // lane quarter
     const int r = q * 32 + lane;           // tile row
+    unsigned char* stg = epi_stage + q * 32 * TC_EPI_PITCH;
     for (int t = 0; t < ntiles; ++t) {
       const int acc = t % TS;
       const uint32_t ph = (t / TS) & 1;
-      if (q == 0) TC_TRACE(3, t);
       mbar_wait(&tfull[acc], ph);
-      if (q == 0) TC_TRACE(4, t);
       tc_fence_after();
       const int64_t gt = g0 + t;
       const int64_t zt = gt / p.tiles_per_z;
       const int64_t grow = (gt - zt * p.tiles_per_z) * 128 + r;
       float2* otile = p.out + zt * p.out_zstride + (grow - lane) * N;   // this warp's 32 rows
       const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * Nr);
-      unsigned char* stg = epi_stage + q * 32 * TC_EPI_PITCH;
       for (int c0 = 0; c0 < Nr; c0 += 32) {
-        const int cols = (c0 + 32 <= Nr) ? 32 : 16;       // real columns in this chunk
+        const int cols = (c0 + 32 <= Nr) ? 32 : 16;
         uint32_t v[32];
         if (cols == 32) {
           tmem_ld32(taddr + c0, v);
@@ -381,15 +382,17 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
           for (int j = 0; j < 16; ++j) v[j] = w16[j];
         }
         tmem_wait_ld();
-        // registers -> padded staging rows (lane = row), conflict-free 16-byte stores
+        if (c0 + 32 >= Nr) {              // accumulator drained: hand it back before the stores
+          tc_fence_before();
+          mbar_arrive_warp(&tempty[acc]);
+        }
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           if (4 * j < cols)
             *reinterpret_cast<uint4*>(stg + lane * TC_EPI_PITCH + j * 16) =
                 make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
         __syncwarp();
-        // staging -> global: 8 (or 4) lanes per row, whole 128-byte lines per instruction
-        const int per_row = cols / 4;                       // 16-byte pieces per row
+        const int per_row = cols / 4;
         if (!(p.dbg & 1)) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
@@ -403,12 +406,9 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
         }
         __syncwarp();
       }
-      tc_fence_before();
-      mbar_arrive_warp(&tempty[acc]);
-      if (q == 0) TC_TRACE(5, t);
     }
   } else if (warp == TC_MMA_WARP) {
-    // ---------------- MMA issuer ----------------
+    // ---------------- MMA issuer (A from TMEM, B from smem) ----------------
     const uint32_t idesc = tf32_idesc(Nr);
     const uint32_t bhi = smem_u32(Bhi), blo = smem_u32(Blo);
     int it = 0;
@@ -417,7 +417,6 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
     for (int t = 0; t < ntiles; ++t) {
       const int64_t zt = (g0 + t) / p.tiles_per_z;
       if (zt != cur_z) {
-        // all MMAs reading the old B' must retire before it is rewritten
         if (lane == 0) umma_commit(bdone);
         __syncwarp();
         mbar_wait(bdone, bdone_phase);
@@ -431,43 +430,35 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
       }
       const int acc = t % TS;
       const uint32_t aph = (t / TS) & 1;
-      TC_TRACE(6, t);
       mbar_wait(&tempty[acc], aph ^ 1);
-      TC_TRACE(7, t);
       tc_fence_after();
       const uint32_t d = tmem + (uint32_t)(acc * Nr);
       for (int c = 0; c < nchunk; ++c, ++it) {
-        const int stage = it % NS;
-        const uint32_t ph = (it / NS) & 1;
+        const int stage = it % AS;
+        const uint32_t ph = (it / AS) & 1;
         mbar_wait(&full[stage], ph);
-        TC_TRACE(8, it);
         tc_fence_after();
         if (lane == 0) {
-          const uint32_t ahi = smem_u32(ring + (size_t)stage * 2 * cbytes);
-          const uint64_t dah0 = umma_desc(ahi, 128, SBO_A);
-          const uint64_t dal0 = umma_desc(ahi + (uint32_t)cbytes, 128, SBO_A);
-          const uint64_t dbh0 = umma_desc(bhi + (uint32_t)(c * units) * 128, 128, SBO_B);
-          const uint64_t dbl0 = umma_desc(blo + (uint32_t)(c * units) * 128, 128, SBO_B);
+          const uint32_t ahi = tmem + A0 + (uint32_t)stage * ACOLS, alo = ahi + 2 * KC;
+          const uint64_t dbh0 = umma_desc(bhi + (uint32_t)(c * KC / 2) * 128, 128, SBO_B);
+          const uint64_t dbl0 = umma_desc(blo + (uint32_t)(c * KC / 2) * 128, 128, SBO_B);
+#pragma unroll
           for (int s = 0; s < KC / 4; ++s) {
-            const uint64_t step = (uint64_t)(s * 256) >> 4;     // start-address field, 16-byte units
-            const uint64_t dah = dah0 + step, dal = dal0 + step;
-            const uint64_t dbh = dbh0 + step, dbl = dbl0 + step;
+            const uint64_t step = (uint64_t)(s * 256) >> 4;     // two 16-byte units of B' per k-step
             const uint32_t first = (c == 0 && s == 0) ? 0u : 1u;
             if (!(p.dbg & 4)) {
-              mma_tf32(d, dal, dbh, idesc, first);   // small terms first
-              mma_tf32(d, dah, dbl, idesc, 1u);
-              mma_tf32(d, dah, dbh, idesc, 1u);
+              mma_tf32_ts(d, alo + 8 * s, dbh0 + step, idesc, first);   // small terms first
+              mma_tf32_ts(d, ahi + 8 * s, dbl0 + step, idesc, 1u);
+              mma_tf32_ts(d, ahi + 8 * s, dbh0 + step, idesc, 1u);
             }
           }
           umma_commit(&empty[stage]);
           if (c == nchunk - 1) umma_commit(&tfull[acc]);
         }
         __syncwarp();
-        TC_TRACE(9, it);
       }
     }
-  }
-  else if (warp == TC_PROD_WARP && RS > 0 && lane == 0) {
+  } else if (warp == TC_PROD_WARP && RS > 0 && lane == 0) {
     // ---------------- raw-ring producer: cp.async.bulk of each tile's segments ----------------
     const uint32_t seg_bytes = (uint32_t)(p.Lseg * 8);
     for (int t = 0; t < ntiles; ++t) {
@@ -484,22 +475,26 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
   __syncthreads();
   if (warp == TC_EPI_WARP0) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(ncols));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
 }
 
 // envelope of the tensor-core kernel
 __host__ inline bool tc_shape_ok(int64_t K, int64_t N, int64_t M) {
-  if (K < 4 || K > 64 || (K % 4) != 0 || (K > 16 && (K % 16) != 0)) return false;
-  if (N < 8 || N > 128 || (N % 8) != 0 || (M % 128) != 0 || M <= 0) return false;
-  return tc_stages_for(K, N, 64) >= 2;
+  if (!(K == 4 || K == 8 || (K % 16) == 0) || K > 64) return false;
+  if (N < 8 || N > 64 || (N % 8) != 0 || (M % 128) != 0 || M <= 0) return false;
+  int TS, AS;
+  tc_tmem_plan(K, N, TS, AS);
+  return AS >= 2 && tc_smem_bytes(K, N, 64, 0) <= 227 * 1024;
 }
 
 // returns 0 if launched, -1 on launch error
 __host__ inline int launch_tc(TcDesc p, int64_t Z, cudaStream_t s) {
   static bool attr_done = false;
   if (!attr_done) {
-    if (cudaFuncSetAttribute(k_tc_c64, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
+    if (cudaFuncSetAttribute(k_tc_c64<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
+        cudaFuncSetAttribute(k_tc_c64<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
+        cudaFuncSetAttribute(k_tc_c64<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
       return -1;
     attr_done = true;
   }
@@ -515,29 +510,28 @@ __host__ inline int launch_tc(TcDesc p, int64_t Z, cudaStream_t s) {
   const int64_t total = Z * p.tiles_per_z;
   int64_t per = (total + sms - 1) / sms;
   if (per < 1) per = 1;
-  while (per > 64 && tc_stages_for(p.K, p.N, per) < 3) per = (per + 1) / 2;   // keep >= 3 ring stages
+  while (per > 256 && tc_smem_bytes(p.K, p.N, per, 2) > 227 * 1024) per = (per + 1) / 2;
   p.per_cta = per;
-  // raw ring when alignment allows and at least 2 raw + 2 A stages fit
+  // raw ring (TMA bulk staging) when alignment allows and >= 2 stages fit
   p.raw_stages = 0;
   const bool aligned = (((uintptr_t)p.a) % 16 == 0) && ((p.a_zstride * 8) % 16 == 0);
   if (p.raw_ok && aligned && !(p.dbg & 256)) {
     for (int rs = 4; rs >= 2; --rs)
-      if (tc_stages_for(p.K, p.N, per, rs) >= 2) { p.raw_stages = rs; break; }
+      if (tc_smem_bytes(p.K, p.N, per, rs) <= 227 * 1024) { p.raw_stages = rs; break; }
   }
-  p.nstages = (int32_t)tc_stages_for(p.K, p.N, per, p.raw_stages);
-  if (p.nstages < 2) return -1;
+  if (tc_smem_bytes(p.K, p.N, per, p.raw_stages) > 227 * 1024) return -1;
+  p.nstages = 0;
   const size_t smem = (size_t)tc_smem_bytes(p.K, p.N, per, p.raw_stages);
-  {
-    const char* st = getenv("TNC_TC_STAGES");
-    if (st && atoi(st) >= 2 && atoi(st) < p.nstages) p.nstages = atoi(st);
-  }
   const int64_t grid = (total + per - 1) / per;     // one wave when per fits in smem
   if (grid <= 0) return 0;
   if (p.dbg & 128) {
     cudaMalloc(&p.trace, 10 * 64 * sizeof(unsigned long long));
     cudaMemset(p.trace, 0, 10 * 64 * sizeof(unsigned long long));
   }
-  k_tc_c64<<<(unsigned)grid, TC_THREADS, smem, s>>>(p);
+  const int kc = (int)tc_kc(p.K);
+  if (kc == 4) k_tc_c64<2><<<(unsigned)grid, TC_THREADS, smem, s>>>(p);
+  else if (kc == 8) k_tc_c64<4><<<(unsigned)grid, TC_THREADS, smem, s>>>(p);
+  else k_tc_c64<8><<<(unsigned)grid, TC_THREADS, smem, s>>>(p);
   if (p.dbg & 128) {
     unsigned long long h[640];
     cudaStreamSynchronize(s);
