@@ -138,10 +138,11 @@ __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.
 // smem sizes (bytes) for a (K, N) problem
 __host__ __device__ inline int64_t tc_b_bytes(int64_t K, int64_t N) { return 2 * (2 * N) * (2 * K) * 4; }
 __host__ __device__ inline int64_t tc_kc(int64_t K) { return K >= 16 ? 16 : K; }
+__host__ __device__ inline int64_t tc_npad(int64_t N) { return N <= 8 ? 8 : ((N + 7) / 8) * 8; }
 constexpr int TC_EPI_PITCH = 144;        // bytes per staged row (128 + 16 pad: conflict-free)
 __host__ __device__ inline int64_t tc_raw_bytes(int64_t K) { return 128 * K * 8; }
 __host__ __device__ inline int64_t tc_smem_bytes(int64_t K, int64_t N, int64_t per, int64_t rs) {
-  return 1024 + tc_b_bytes(K, N) + K * 8 + K * 4 + 128 * 8 + 6 * TC_MAX_STAGES * 8 + 128 + per * 8
+  return 1024 + tc_b_bytes(K, tc_npad(N)) + K * 8 + K * 4 + 128 * 8 + 6 * TC_MAX_STAGES * 8 + 128 + per * 8
          + 4 * 32 * TC_EPI_PITCH + 16 + rs * tc_raw_bytes(K);
 }
 // TMEM plan: TS accumulators of Nr columns, AS A-chunk stages of 4*KC columns (hi + lo)
@@ -208,12 +209,13 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   constexpr int KC = 2 * KH;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int K = (int)p.K, N = (int)p.N;
-  const int Kr = 2 * K, Nr = 2 * N;
+  const int K = (int)p.K, N = (int)p.N;          // N: real outputs per row
+  const int Np = (int)tc_npad(p.N);              // MMA width (multiple of 8, >= 8)
+  const int Kr = 2 * K, Nr = 2 * Np;
   const int nchunk = K / KC;
   const uint32_t SBO_B = (Kr / 4) * 128;
   int TS, AS;
-  tc_tmem_plan(p.K, p.N, TS, AS);
+  tc_tmem_plan(p.K, Np, TS, AS);
   const uint32_t A0 = (uint32_t)(TS * Nr);      // first A column
   constexpr uint32_t ACOLS = 4 * KC;            // per A stage: hi (2KC) + lo (2KC)
   // ---- shared memory carve-up ----
@@ -268,6 +270,11 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
   for (int k = threadIdx.x; k < K; k += blockDim.x) akoff_s[k] = p.rows_contig ? k : p.akoff[k];
   for (int r = threadIdx.x; r < 128; r += blockDim.x) looff_s[r] = p.rows_contig ? (int64_t)r * K : p.lo_off[r];
   for (int k = threadIdx.x; k < K && RS > 0; k += blockDim.x) kraw_s[k] = p.rows_contig ? k : p.kraw[k];
+  if (Np != N) {
+    uint4* bz = reinterpret_cast<uint4*>(Bhi);
+    for (int i = threadIdx.x; i < 2 * Nr * Kr / 4; i += blockDim.x) bz[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+  }
   if (ntiles > 0) build_b(p, z0, Bhi, Blo, threadIdx.x, blockDim.x);
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
     const int64_t g = g0 + t;
@@ -392,8 +399,9 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
             *reinterpret_cast<uint4*>(stg + lane * TC_EPI_PITCH + j * 16) =
                 make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
         __syncwarp();
-        const int per_row = cols / 4;
-        if (!(p.dbg & 1)) {
+        const int real = min(cols, 2 * N - c0);        // real (unpadded) columns in this chunk
+        const int per_row = real / 4;
+        if (!(p.dbg & 1) && per_row > 0) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int idx = i * 32 + lane;
@@ -482,9 +490,9 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
 // envelope of the tensor-core kernel
 __host__ inline bool tc_shape_ok(int64_t K, int64_t N, int64_t M) {
   if (!(K == 4 || K == 8 || (K % 16) == 0) || K > 64) return false;
-  if (N < 8 || N > 64 || (N % 8) != 0 || (M % 128) != 0 || M <= 0) return false;
+  if (N < 2 || N > 64 || (N % 2) != 0 || (N > 8 && (N % 8) != 0) || (M % 128) != 0 || M <= 0) return false;
   int TS, AS;
-  tc_tmem_plan(K, N, TS, AS);
+  tc_tmem_plan(K, tc_npad(N), TS, AS);
   return AS >= 2 && tc_smem_bytes(K, N, 64, 0) <= 227 * 1024;
 }
 

@@ -13,7 +13,7 @@ def rel_l2(got, ref):
 
 
 @pytest.mark.parametrize("r,k,n,B", [(7, 1, 2, 2), (7, 2, 2, 3), (8, 3, 3, 2), (9, 1, 3, 2), (9, 3, 2, 3),
-                                     (10, 2, 3, 1), (11, 3, 3, 1), (7, 3, 2, 1)])
+                                     (10, 2, 3, 1), (11, 3, 3, 1), (7, 3, 2, 1), (8, 3, 1, 3), (9, 3, 1, 1)])
 def test_tc_pair_matches_oracle(r, k, n, B):
     import torch
 
