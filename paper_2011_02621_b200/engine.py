@@ -403,11 +403,14 @@ class PathExecutor:
                     out.append((b0, 1, s0, min(self.max_z, slices.stop - s0)))
         return out
 
-    def run(self, sel, B: int, amp, slices: range | None = None, stream=None, accumulate=False):
-        """Contract all bitstrings x ``slices``; writes (or adds) into ``amp``.
+    def run(self, sel, B: int, amp, slices: range | None = None, stream=None, accumulate=False,
+            b_offset: int = 0):
+        """Contract bitstrings [b_offset, b_offset + B) x ``slices``; writes (or
+        adds, ``accumulate``) into ``amp[b_offset:b_offset + B]``.
 
-        sel: dict node -> device int32 tensor [B] of variant indices (None for
-        single-variant sites); amp: device tensor [B] of the engine dtype.
+        sel: dict node -> device int32 tensor of variant indices over the whole
+        batch (None for single-variant sites); amp: device tensor of the engine
+        dtype.
         """
         torch = self.torch
         plan = self.plan
@@ -420,6 +423,7 @@ class PathExecutor:
         pd = self._pd
         q0 = plan.path[0]
         for ci, (b0, nb, s0, ns) in enumerate(self.chunks(B, slices)):
+            b0 += b_offset
             z = nb * ns
             bufa, bufb = self._buffers(z)
             cur, nxt = bufa, bufb
