@@ -66,14 +66,32 @@ __device__ __forceinline__ void mbar_arrive_warp(uint64_t* bar) {
   __syncwarp();
   if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
 }
+#ifndef TNC_MBAR_HINT
+#define TNC_MBAR_HINT 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+#if TNC_MBAR_HINT
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
       "@P1 bra DONE_%=;\n\t"
       "bra WAIT_%=;\n\t"
-      "DONE_%=:\n\t}" ::"r"(smem_u32(bar)), "r"(phase), "r"(0x989680) : "memory");
+      "DONE_%=:\n\t}" ::"r"(smem_u32(bar)), "r"(phase), "r"(TNC_MBAR_HINT) : "memory");
+#else
+  // try_wait + nanosleep backoff: a waiting warp does not steal issue slots
+  // from the working warps of its SM sub-partition
+  uint32_t done = 0, ns = 8;
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}" : "=r"(done) : "r"(smem_u32(bar)), "r"(phase) : "memory");
+    if (done) break;
+    __nanosleep(ns);
+    if (ns < 256) ns <<= 1;
+  }
+#endif
 }
 // global -> shared bulk copy completing on `bar` (16-byte aligned, size % 16 == 0)
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {

@@ -69,11 +69,14 @@ __device__ __forceinline__ uint32_t tf32_rna(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return r;
 }
-// hi = tf32(x), lo = tf32(x - hi)
+// hi = x with the 13 low mantissa bits cleared (exactly representable in tf32),
+// lo = x - hi (exact in fp32; the tensor core reads its top 19 bits).  Two
+// instructions per value -- the cvt.rna.tf32 path costs ~8 SASS instructions
+// and made the converter warps issue-bound.  Dropped terms: lo*lo and the
+// truncation of lo, both <= 2^-21 relative.
 __device__ __forceinline__ void split3(float x, float& hi, float& lo) {
-  const uint32_t h = tf32_rna(x);
-  hi = __uint_as_float(h);
-  lo = __uint_as_float(tf32_rna(x - hi));
+  hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+  lo = x - hi;
 }
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -163,9 +166,17 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, ui
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}"
       ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
-template <int NW>
-__device__ __forceinline__ void tmem_st(uint32_t taddr, const uint32_t (&v)[16]) {
-  if constexpr (NW == 16) {
+template <int NW, int LEN>
+__device__ __forceinline__ void tmem_st(uint32_t taddr, const uint32_t (&v)[LEN]) {
+  static_assert(NW <= LEN, "tmem_st width");
+  if constexpr (NW == 32) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+                 "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+                 ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+                   "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]),
+                   "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]),
+                   "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31]));
+  } else if constexpr (NW == 16) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};"
                  ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
                    "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]));
@@ -248,7 +259,7 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
   // ---- setup ----
   if (threadIdx.x == 0) {
     for (int s = 0; s < AS; ++s) {
-      mbar_init(&full[s], TC_CONV_WARPS);
+      mbar_init(&full[s], 4);
       mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < TS; ++s) {
@@ -257,7 +268,7 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
     }
     for (int s = 0; s < RS; ++s) {
       mbar_init(&rfull[s], 1);
-      mbar_init(&rempty[s], TC_CONV_WARPS);
+      mbar_init(&rempty[s], 4);
     }
     mbar_init(bdone, 1);
     mbar_fence_init();
@@ -299,68 +310,65 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
   const uint32_t tmem = *tmem_slot;
 
   if (warp < TC_CONV_WARPS) {
-    // ---------------- converters: row r = tid % 128 (TMEM lane), half h = tid / 128 ----------------
-    const int r = threadIdx.x & 127, h = threadIdx.x >> 7;
+    // ---------------- converters: 2 groups of 4 warps alternate tiles; thread =
+    // one tile row (TMEM lane) and all KC values of a chunk ----------------
+    // Each group owns its own slice of the A ring (stages [grp*ASg, (grp+1)*ASg))
+    // and, with RS even, its own raw stages, so no waiter can alias a barrier
+    // phase two uses ahead.
+    const int NG = (AS >= 4 && (RS == 0 || RS % 2 == 0)) ? 2 : 1;
+    const int grp = warp >> 2;
+    const int ASg = AS / NG;
+    const int r = (warp & 3) * 32 + lane;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     const float2* A = p.a + looff_s[r];
-    const int total = ntiles * nchunk;
-    auto load = [&](float2 (&v)[KH], int it) {
-      if (it >= total || RS > 0) return;
-      const int t = it / nchunk, c = it - t * nchunk;
-      const float2* Ar = A + tbase[t];
-      const int64_t* ko = akoff_s + c * KC + h * KH;
-#pragma unroll
-      for (int q = 0; q < KH; ++q) v[q] = __ldg(Ar + ko[q]);
-    };
-    auto store = [&](const float2 (&vin)[KH], int it) {
-      const int stage = it % AS;
-      const uint32_t ph = (it / AS) & 1;
-      const int tt = it / nchunk, cc = it - tt * nchunk;
-      float2 v[KH];
+    int j = 0;                                   // this group's chunk counter
+    for (int t = grp; t < ntiles && grp < NG; t += NG) {
+      const float2* raw = nullptr;
+      if ((warp & 3) == 0) TC_TRACE(0, t);
       if (RS > 0) {
-        const int rs = tt % RS;
-        if (cc == 0) mbar_wait(&rfull[rs], (uint32_t)((tt / RS) & 1));
-        const float2* raw = reinterpret_cast<const float2*>(rawring + (size_t)rs * tc_raw_bytes(p.K)) + looff_s[r];
-        const int32_t* kr = kraw_s + cc * KC + h * KH;
-#pragma unroll
-        for (int q = 0; q < KH; ++q) v[q] = raw[kr[q]];
-      } else {
-#pragma unroll
-        for (int q = 0; q < KH; ++q) v[q] = vin[q];
+        const int rs = t % RS;
+        mbar_wait(&rfull[rs], (uint32_t)((t / RS) & 1));
+        if ((warp & 3) == 0) TC_TRACE(1, t);
+        raw = reinterpret_cast<const float2*>(rawring + (size_t)rs * tc_raw_bytes(p.K)) + looff_s[r];
       }
-      uint32_t hi[16], lo[16];
+      const float2* Ar = A + tbase[t];
+      for (int c = 0; c < nchunk; ++c, ++j) {
+        const int stage = grp * ASg + j % ASg;
+        const uint32_t ph = (j / ASg) & 1;
+        float2 v[KC];
+        if (RS > 0) {
+          const int32_t* kr = kraw_s + c * KC;
 #pragma unroll
-      for (int q = 0; q < KH; ++q) {
-        float a, b;
-        split3(v[q].x, a, b);
-        hi[2 * q] = __float_as_uint(a);
-        lo[2 * q] = __float_as_uint(b);
-        split3(v[q].y, a, b);
-        hi[2 * q + 1] = __float_as_uint(a);
-        lo[2 * q + 1] = __float_as_uint(b);
+          for (int q = 0; q < KC; ++q) v[q] = raw[kr[q]];
+          if (c == nchunk - 1) mbar_arrive_warp(&rempty[t % RS]);   // this tile's raw values are in registers
+        } else {
+          const int64_t* ko = akoff_s + c * KC;
+#pragma unroll
+          for (int q = 0; q < KC; ++q) v[q] = (p.dbg & 2) ? make_float2(1.f, 0.f) : __ldg(Ar + ko[q]);
+        }
+        uint32_t hi[2 * KC], lo[2 * KC];
+#pragma unroll
+        for (int q = 0; q < KC; ++q) {
+          float a, b;
+          split3(v[q].x, a, b);
+          hi[2 * q] = __float_as_uint(a);
+          lo[2 * q] = __float_as_uint(b);
+          split3(v[q].y, a, b);
+          hi[2 * q + 1] = __float_as_uint(a);
+          lo[2 * q + 1] = __float_as_uint(b);
+        }
+        mbar_wait(&empty[stage], ph ^ 1);
+        tc_fence_after();
+        const uint32_t col = A0 + (uint32_t)stage * ACOLS;
+        if (!(p.dbg & 512)) {
+          tmem_st<2 * KC>(tmem + lane_base + col, hi);
+          tmem_st<2 * KC>(tmem + lane_base + col + 2 * KC, lo);
+          tmem_wait_st();
+        }
+        tc_fence_before();
+        mbar_arrive_warp(&full[stage]);
+        if ((warp & 3) == 0 && c == nchunk - 1) TC_TRACE(2, t);
       }
-      if (RS > 0 && cc == nchunk - 1) mbar_arrive_warp(&rempty[tt % RS]);   // raw values are in registers
-      mbar_wait(&empty[stage], ph ^ 1);
-      tc_fence_after();
-      const uint32_t col = A0 + (uint32_t)stage * ACOLS + (uint32_t)(h * 2 * KH);
-      tmem_st<2 * KH>(tmem + lane_base + col, hi);
-      tmem_st<2 * KH>(tmem + lane_base + col + 2 * KC, lo);
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive_warp(&full[stage]);
-    };
-    float2 v0[KH], v1[KH], v2[KH];
-    load(v0, 0);
-    load(v1, 1);
-    for (int it = 0; it < total; it += 3) {
-      load(v2, it + 2);
-      store(v0, it);
-      if (it + 1 >= total) break;
-      load(v0, it + 3);
-      store(v1, it + 1);
-      if (it + 2 >= total) break;
-      load(v1, it + 4);
-      store(v2, it + 2);
     }
   } else if (warp < TC_MMA_WARP) {
     // ---------------- epilogue: TMEM -> registers -> padded smem -> coalesced global ----------------
@@ -370,7 +378,9 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
     for (int t = 0; t < ntiles; ++t) {
       const int acc = t % TS;
       const uint32_t ph = (t / TS) & 1;
+      if (q == 0) TC_TRACE(3, t);
       mbar_wait(&tfull[acc], ph);
+      if (q == 0) TC_TRACE(4, t);
       tc_fence_after();
       const int64_t gt = g0 + t;
       const int64_t zt = gt / p.tiles_per_z;
@@ -380,7 +390,10 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
       for (int c0 = 0; c0 < Nr; c0 += 32) {
         const int cols = (c0 + 32 <= Nr) ? 32 : 16;
         uint32_t v[32];
-        if (cols == 32) {
+        if (p.dbg & 1024) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = j;
+        } else if (cols == 32) {
           tmem_ld32(taddr + c0, v);
         } else {
           uint32_t w16[16];
@@ -389,6 +402,7 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
           for (int j = 0; j < 16; ++j) v[j] = w16[j];
         }
         tmem_wait_ld();
+        if (q == 0 && c0 == 0) TC_TRACE(14, t);
         if (c0 + 32 >= Nr) {              // accumulator drained: hand it back before the stores
           tc_fence_before();
           mbar_arrive_warp(&tempty[acc]);
@@ -399,6 +413,7 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
             *reinterpret_cast<uint4*>(stg + lane * TC_EPI_PITCH + j * 16) =
                 make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
         __syncwarp();
+        if (q == 0 && c0 == 0) TC_TRACE(15, t);
         const int real = min(cols, 2 * N - c0);        // real (unpadded) columns in this chunk
         const int per_row = real / 4;
         if (!(p.dbg & 1) && per_row > 0) {
@@ -414,6 +429,7 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
         }
         __syncwarp();
       }
+      if (q == 0) TC_TRACE(5, t);
     }
   } else if (warp == TC_MMA_WARP) {
     // ---------------- MMA issuer (A from TMEM, B from smem) ----------------
@@ -438,13 +454,20 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
       }
       const int acc = t % TS;
       const uint32_t aph = (t / TS) & 1;
+      TC_TRACE(6, t);
       mbar_wait(&tempty[acc], aph ^ 1);
+      TC_TRACE(7, t);
       tc_fence_after();
       const uint32_t d = tmem + (uint32_t)(acc * Nr);
       for (int c = 0; c < nchunk; ++c, ++it) {
-        const int stage = it % AS;
-        const uint32_t ph = (it / AS) & 1;
+        const int NGm = (AS >= 4 && (RS == 0 || RS % 2 == 0)) ? 2 : 1;
+        const int ASg = AS / NGm;
+        const int g = t % NGm;
+        const int jj = (t / NGm) * nchunk + c;
+        const int stage = g * ASg + jj % ASg;
+        const uint32_t ph = (jj / ASg) & 1;
         mbar_wait(&full[stage], ph);
+        TC_TRACE(8, it);
         tc_fence_after();
         if (lane == 0) {
           const uint32_t ahi = tmem + A0 + (uint32_t)stage * ACOLS, alo = ahi + 2 * KC;
@@ -464,6 +487,7 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
           if (c == nchunk - 1) umma_commit(&tfull[acc]);
         }
         __syncwarp();
+        TC_TRACE(9, it);
       }
     }
   } else if (warp == TC_PROD_WARP && RS > 0 && lane == 0) {
@@ -471,7 +495,9 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
     const uint32_t seg_bytes = (uint32_t)(p.Lseg * 8);
     for (int t = 0; t < ntiles; ++t) {
       const int rs = t % RS;
+      TC_TRACE(12, t);
       mbar_wait(&rempty[rs], (uint32_t)(((t / RS) & 1) ^ 1));
+      TC_TRACE(13, t);
       unsigned char* dst = rawring + (size_t)rs * tc_raw_bytes(p.K);
       const float2* src = p.a + tbase[t];
       mbar_expect_tx(&rfull[rs], (uint32_t)(p.Kout * seg_bytes));
@@ -524,7 +550,9 @@ __host__ inline int launch_tc(TcDesc p, int64_t Z, cudaStream_t s) {
   p.raw_stages = 0;
   const bool aligned = (((uintptr_t)p.a) % 16 == 0) && ((p.a_zstride * 8) % 16 == 0);
   if (p.raw_ok && aligned && !(p.dbg & 256)) {
-    for (int rs = 4; rs >= 2; --rs)
+    int rs_max = 4;
+    if (const char* e = getenv("TNC_TC_RS")) rs_max = atoi(e);
+    for (int rs = rs_max & ~1; rs >= 2; rs -= 2)
       if (tc_smem_bytes(p.K, p.N, per, rs) <= 227 * 1024) { p.raw_stages = rs; break; }
   }
   if (tc_smem_bytes(p.K, p.N, per, p.raw_stages) > 227 * 1024) return -1;
@@ -533,23 +561,25 @@ __host__ inline int launch_tc(TcDesc p, int64_t Z, cudaStream_t s) {
   const int64_t grid = (total + per - 1) / per;     // one wave when per fits in smem
   if (grid <= 0) return 0;
   if (p.dbg & 128) {
-    cudaMalloc(&p.trace, 10 * 64 * sizeof(unsigned long long));
-    cudaMemset(p.trace, 0, 10 * 64 * sizeof(unsigned long long));
+    cudaMalloc(&p.trace, 18 * 64 * sizeof(unsigned long long));
+    cudaMemset(p.trace, 0, 18 * 64 * sizeof(unsigned long long));
   }
   const int kc = (int)tc_kc(p.K);
   if (kc == 4) k_tc_c64<2><<<(unsigned)grid, TC_THREADS, smem, s>>>(p);
   else if (kc == 8) k_tc_c64<4><<<(unsigned)grid, TC_THREADS, smem, s>>>(p);
   else k_tc_c64<8><<<(unsigned)grid, TC_THREADS, smem, s>>>(p);
   if (p.dbg & 128) {
-    unsigned long long h[640];
+    unsigned long long h[18 * 64];
     cudaStreamSynchronize(s);
     cudaMemcpy(h, p.trace, sizeof h, cudaMemcpyDeviceToHost);
     const unsigned long long t0 = h[0];
-    const char* names[10] = {"conv_pre_empty", "conv_got_empty", "conv_arrived", "epi_pre_tfull", "epi_got_tfull",
-                             "epi_arrived", "mma_pre_tempty", "mma_got_tempty", "mma_got_full", "mma_committed"};
-    for (int sl = 0; sl < 10; ++sl) {
+    const char* names[18] = {"conv_pre_empty", "conv_got_empty", "conv_arrived", "epi_pre_tfull", "epi_got_tfull",
+                             "epi_done", "mma_pre_tempty", "mma_got_tempty", "mma_got_full", "mma_committed",
+                             "conv_pre_raw", "conv_got_raw", "prod_pre_rempty", "prod_got_rempty",
+                             "epi_ld_done", "epi_sts_done", "conv_lds_done", "conv_st_done"};
+    for (int sl = 0; sl < 18; ++sl) {
       printf("%-16s", names[sl]);
-      for (int t = 0; t < 24; ++t) printf(" %6lld", h[sl * 64 + t] ? (long long)(h[sl * 64 + t] - t0) : -1LL);
+      for (int t = 0; t < 20; ++t) printf(" %6lld", h[sl * 64 + t] ? (long long)(h[sl * 64 + t] - t0) : -1LL);
       printf("\n");
     }
     cudaFree(p.trace);
