@@ -12,6 +12,7 @@
 #include "tnc_kernels.cuh"
 #include "tnc_pair.cuh"
 #include "tnc_tc.cuh"
+#include "tnc_dmma.cuh"
 
 namespace {
 
@@ -111,7 +112,7 @@ int launch_step(const tnc_step_desc& d, cudaStream_t s) {
   if (d.site.ncut < 0 || d.site.ncut > TNC_MAX_CUTS) return fail(TNC_E_INVALID, "tnc_step: ncut=%d", d.site.ncut);
   int kernel = d.kernel;
   if (kernel == TNC_K_TC || (kernel == TNC_K_AUTO && tc_enabled())) {
-    int rc = tnc::try_tc<R>(d, s);
+    int rc = sizeof(R) == 8 ? tnc::try_dmma<R>(d, s) : tnc::try_tc<R>(d, s);
     if (rc == 1) return check_launch("tnc_step[tc]");
     if (rc < 0) return check_launch("tnc_step[tc] launch");
     if (kernel == TNC_K_TC) return fail(TNC_E_UNSUPPORTED, "tnc_step: shape outside the tensor-core kernel envelope");

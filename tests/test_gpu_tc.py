@@ -60,3 +60,35 @@ def test_tc_engine_step_contiguous():
     kn = [(sp.K, sp.N, sp.M, sp.c_rows_contig) for sp in e64.plan.steps]
     got = e64.amplitudes(outs)
     assert rel_l2(got, ref) <= 1e-4, (rel_l2(got, ref), kn)
+
+
+@pytest.mark.parametrize("dtype,tol", [("complex128", 1e-12), ("complex64", 1e-5)])
+@pytest.mark.parametrize("V", [1, 3])
+def test_engine_tensor_core_steps(dtype, tol, V):
+    """Engine steps with K*N >= 256 run on the tensor cores (DMMA for
+    complex128, tcgen05 3xTF32 for complex64); chain 0-1-2 plus a closing
+    edge, checked against the numpy oracle per variant."""
+    import torch
+
+    from paper_2011_02621_b200.engine import ContractionPlan, NetworkSpec, PathExecutor
+
+    rng = np.random.default_rng(7 + V)
+    edges = {(0, 1): 64, (1, 2): 32, (0, 2): 128, (2, 3): 4, (0, 3): 2}
+    legs = {0: [(0, 1), (0, 2), (0, 3)], 1: [(0, 1), (1, 2)], 2: [(0, 2), (1, 2), (2, 3)], 3: [(0, 3), (2, 3)]}
+    spec = NetworkSpec([0, 1, 2, 3], edges, legs)
+    sites = {}
+    for q in range(4):
+        dims = spec.site_dims(q)
+        sites[q] = (rng.standard_normal((V,) + dims) + 1j * rng.standard_normal((V,) + dims)) / np.sqrt(np.prod(dims))
+    plan = ContractionPlan(spec, [0, 1, 2, 3])
+    assert any(sp.K * sp.N >= 256 and sp.M % 128 == 0 for sp in plan.steps)
+    ex = PathExecutor(plan, {q: torch.from_numpy(sites[q]) for q in range(4)}, dtype=dtype)
+    B = 4
+    bits = rng.integers(0, V, (B, 4)).astype(np.int32)
+    sel = {q: torch.from_numpy(np.ascontiguousarray(bits[:, q])).cuda() for q in range(4)}
+    amp = torch.zeros(B, dtype=ex.tdtype, device="cuda")
+    ex.run(sel, B, amp)
+    got = amp.cpu().numpy().astype(np.complex128)
+    ref = np.array([O.contract_along_path({q: (sites[q][bits[b, q]], legs[q]) for q in range(4)}, [0, 1, 2, 3])[0]
+                    for b in range(B)])
+    assert rel_l2(got, ref) <= tol
