@@ -63,6 +63,7 @@ typedef struct {
   const int32_t* sel;
   int64_t        zstride;
   int64_t        vstride;
+  int64_t        nvariants;   /* number of variants behind sel (0 = unknown) */
   int32_t        ncut;
   int32_t        _pad;
   int64_t        cut_stride[TNC_MAX_CUTS];

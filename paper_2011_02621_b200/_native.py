@@ -35,7 +35,7 @@ class NativeError(RuntimeError):
 class Site(C.Structure):
     _fields_ = [
         ("ptr", C.c_void_p), ("sel", C.c_void_p), ("zstride", C.c_int64), ("vstride", C.c_int64),
-        ("ncut", C.c_int32), ("_pad", C.c_int32),
+        ("nvariants", C.c_int64), ("ncut", C.c_int32), ("_pad", C.c_int32),
         ("cut_stride", C.c_int64 * MAX_CUTS), ("cut_div", C.c_int64 * MAX_CUTS),
         ("cut_ext", C.c_int64 * MAX_CUTS),
     ]

@@ -13,20 +13,26 @@
 #include "tnc_pair.cuh"
 #include "tnc_tc.cuh"
 #include "tnc_dmma.cuh"
+#include "tnc_tcgemm.cuh"
 
 namespace {
 
 thread_local std::string g_err;
 
-// TNC_KERNELS=simt disables the tensor-core path (tests compare both)
-bool tc_enabled() {
+// TNC_KERNELS=simt disables the tensor-core paths (tests compare both);
+// "tc-resident" / "tc-gemm" keep only one of them (precision probes).
+int tc_mask() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("TNC_KERNELS");
-    v = (e && strcmp(e, "simt") == 0) ? 0 : 1;
+    v = 3;
+    if (e && strcmp(e, "simt") == 0) v = 0;
+    if (e && strcmp(e, "tc-resident") == 0) v = 1;
+    if (e && strcmp(e, "tc-gemm") == 0) v = 2;
   }
-  return v == 1;
+  return v;
 }
+bool tc_enabled() { return tc_mask() != 0; }
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -112,7 +118,10 @@ int launch_step(const tnc_step_desc& d, cudaStream_t s) {
   if (d.site.ncut < 0 || d.site.ncut > TNC_MAX_CUTS) return fail(TNC_E_INVALID, "tnc_step: ncut=%d", d.site.ncut);
   int kernel = d.kernel;
   if (kernel == TNC_K_TC || (kernel == TNC_K_AUTO && tc_enabled())) {
-    int rc = sizeof(R) == 8 ? tnc::try_dmma<R>(d, s) : tnc::try_tc<R>(d, s);
+    const int mask = kernel == TNC_K_TC ? 3 : tc_mask();
+    int rc = 0;
+    if (mask & 1) rc = sizeof(R) == 8 ? tnc::try_dmma<R>(d, s) : tnc::try_tc<R>(d, s);
+    if (rc == 0 && (mask & 2) && sizeof(R) == 4) rc = tnc::try_tc_gemm<R>(d, s);
     if (rc == 1) return check_launch("tnc_step[tc]");
     if (rc < 0) return check_launch("tnc_step[tc] launch");
     if (kernel == TNC_K_TC) return fail(TNC_E_UNSUPPORTED, "tnc_step: shape outside the tensor-core kernel envelope");
@@ -642,7 +651,7 @@ void bind_tables(tnc_pair_plan& P, void* dev) {
 int execute_pair_plan(const tnc_pair_plan& P, int64_t batch, const void* a, int64_t a_zstride, const void* b,
                       int64_t b_zstride, void* out, int64_t out_zstride, cudaStream_t s) {
   if (batch <= 0) return TNC_OK;
-  if (P.tc_ok && tc_enabled() && P.tc.K * P.tc.N >= 256) {
+  if (P.tc_ok && (tc_mask() & 1) && P.tc.K * P.tc.N >= 256) {
     tnc::TcDesc c = P.tc;
     c.a = reinterpret_cast<const float2*>(a);
     c.a_zstride = a_zstride;
@@ -735,7 +744,7 @@ int tnc_pair_plan_execute(const tnc_pair_plan* plan, int64_t batch, const void* 
 
 int tnc_pair_plan_kernel(const tnc_pair_plan* plan) {
   if (!plan) return TNC_E_INVALID;
-  if (plan->tc_ok && tc_enabled() && plan->tc.K * plan->tc.N >= 256) return TNC_K_TC;
+  if (plan->tc_ok && (tc_mask() & 1) && plan->tc.K * plan->tc.N >= 256) return TNC_K_TC;
   return plan->kind;
 }
 

@@ -58,9 +58,10 @@ struct TcDesc {
 
 constexpr int TC_CONV_WARPS = 8;
 constexpr int TC_EPI_WARP0 = 8;
-constexpr int TC_MMA_WARP = 12;
-constexpr int TC_PROD_WARP = 13;         // raw-ring producer (cp.async.bulk)
-constexpr int TC_THREADS = 14 * 32;
+constexpr int TC_EPI_WARPS = 8;          // two epilogue groups alternate tiles
+constexpr int TC_MMA_WARP = 16;
+constexpr int TC_PROD_WARP = 17;         // raw-ring producer (cp.async.bulk)
+constexpr int TC_THREADS = 18 * 32;
 constexpr int TC_MAX_STAGES = 8;
 constexpr int TC_MAX_TILES = 2048;      // tiles per CTA (one wave; smem base table)
 
@@ -69,13 +70,14 @@ __device__ __forceinline__ uint32_t tf32_rna(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return r;
 }
-// hi = x with the 13 low mantissa bits cleared (exactly representable in tf32),
-// lo = x - hi (exact in fp32; the tensor core reads its top 19 bits).  Two
-// instructions per value -- the cvt.rna.tf32 path costs ~8 SASS instructions
-// and made the converter warps issue-bound.  Dropped terms: lo*lo and the
-// truncation of lo, both <= 2^-21 relative.
+// hi = x rounded to the nearest tf32 (add half an ulp, clear the 13 low
+// mantissa bits), lo = x - hi (exact in fp32; the tensor core reads its top 19
+// bits).  Rounding hi to nearest keeps lo sign-random, so the dropped lo*lo
+// term and the truncation of lo do not correlate with the sign of a*b and
+// cancel in long sums (a truncated hi biases every product by ~2^-23).
+// Three instructions per value (cvt.rna.tf32 expands to ~8).
 __device__ __forceinline__ void split3(float x, float& hi, float& lo) {
-  hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+  hi = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
   lo = x - hi;
 }
 
@@ -146,13 +148,14 @@ constexpr int TC_EPI_PITCH = 144;        // bytes per staged row (128 + 16 pad: 
 __host__ __device__ inline int64_t tc_raw_bytes(int64_t K) { return 128 * K * 8; }
 __host__ __device__ inline int64_t tc_smem_bytes(int64_t K, int64_t N, int64_t per, int64_t rs) {
   return 1024 + tc_b_bytes(K, tc_npad(N)) + K * 8 + K * 4 + 128 * 8 + 6 * TC_MAX_STAGES * 8 + 128 + per * 8
-         + 4 * 32 * TC_EPI_PITCH + 16 + rs * tc_raw_bytes(K);
+         + TC_EPI_WARPS * 32 * TC_EPI_PITCH + 16 + rs * tc_raw_bytes(K);
 }
 // TMEM plan: TS accumulators of Nr columns, AS A-chunk stages of 4*KC columns (hi + lo)
 __host__ __device__ inline void tc_tmem_plan(int64_t K, int64_t N, int& TS, int& AS) {
   const int Nr = (int)(2 * N), kc = (int)tc_kc(K);
   TS = 256 / Nr;
   if (TS > TC_MAX_STAGES) TS = TC_MAX_STAGES;
+  TS &= ~1;                                     // even: each epilogue group owns its stages
   if (TS < 2) TS = 2;
   AS = (512 - TS * Nr) / (4 * kc);
   if (AS > TC_MAX_STAGES) AS = TC_MAX_STAGES;
@@ -346,25 +349,28 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
 #pragma unroll
           for (int q = 0; q < KC; ++q) v[q] = (p.dbg & 2) ? make_float2(1.f, 0.f) : __ldg(Ar + ko[q]);
         }
-        uint32_t hi[2 * KC], lo[2 * KC];
-#pragma unroll
-        for (int q = 0; q < KC; ++q) {
-          float a, b;
-          split3(v[q].x, a, b);
-          hi[2 * q] = __float_as_uint(a);
-          lo[2 * q] = __float_as_uint(b);
-          split3(v[q].y, a, b);
-          hi[2 * q + 1] = __float_as_uint(a);
-          lo[2 * q + 1] = __float_as_uint(b);
-        }
         mbar_wait(&empty[stage], ph ^ 1);
         tc_fence_after();
         const uint32_t col = A0 + (uint32_t)stage * ACOLS;
-        if (!(p.dbg & 512)) {
-          tmem_st<2 * KC>(tmem + lane_base + col, hi);
-          tmem_st<2 * KC>(tmem + lane_base + col + 2 * KC, lo);
-          tmem_wait_st();
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          uint32_t hi[KC], lo[KC];
+#pragma unroll
+          for (int q = 0; q < KC / 2; ++q) {
+            float a, b;
+            split3(v[half * KC / 2 + q].x, a, b);
+            hi[2 * q] = __float_as_uint(a);
+            lo[2 * q] = __float_as_uint(b);
+            split3(v[half * KC / 2 + q].y, a, b);
+            hi[2 * q + 1] = __float_as_uint(a);
+            lo[2 * q + 1] = __float_as_uint(b);
+          }
+          if (!(p.dbg & 512)) {
+            tmem_st<KC>(tmem + lane_base + col + half * KC, hi);
+            tmem_st<KC>(tmem + lane_base + col + 2 * KC + half * KC, lo);
+          }
         }
+        if (!(p.dbg & 512)) tmem_wait_st();
         tc_fence_before();
         mbar_arrive_warp(&full[stage]);
         if ((warp & 3) == 0 && c == nchunk - 1) TC_TRACE(2, t);
@@ -372,10 +378,11 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
     }
   } else if (warp < TC_MMA_WARP) {
     // ---------------- epilogue: TMEM -> registers -> padded smem -> coalesced global ----------------
-    const int q = warp - TC_EPI_WARP0;     // lane quarter
-    const int r = q * 32 + lane;           // tile row
-    unsigned char* stg = epi_stage + q * 32 * TC_EPI_PITCH;
-    for (int t = 0; t < ntiles; ++t) {
+    const int eg = (warp - TC_EPI_WARP0) >> 2;   // epilogue group (alternate tiles; TS even)
+    const int q = warp & 3;                      // lane quarter
+    const int r = q * 32 + lane;                 // tile row
+    unsigned char* stg = epi_stage + (eg * 4 + q) * 32 * TC_EPI_PITCH;
+    for (int t = eg; t < ntiles; t += 2) {
       const int acc = t % TS;
       const uint32_t ph = (t / TS) & 1;
       if (q == 0) TC_TRACE(3, t);
@@ -477,7 +484,9 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
           for (int s = 0; s < KC / 4; ++s) {
             const uint64_t step = (uint64_t)(s * 256) >> 4;     // two 16-byte units of B' per k-step
             const uint32_t first = (c == 0 && s == 0) ? 0u : 1u;
-            if (!(p.dbg & 4)) {
+            if (p.dbg & 2048) {
+              mma_tf32_ts(d, ahi + 8 * s, dbh0 + step, idesc, first);    // timing experiment: 1xTF32
+            } else if (!(p.dbg & 4)) {
               mma_tf32_ts(d, alo + 8 * s, dbh0 + step, idesc, first);   // small terms first
               mma_tf32_ts(d, ahi + 8 * s, dbl0 + step, idesc, 1u);
               mma_tf32_ts(d, ahi + 8 * s, dbh0 + step, idesc, 1u);

@@ -240,11 +240,12 @@ def _site_cut_info(plan: ContractionPlan, layout: Sequence[Edge], dims: Sequence
     return info
 
 
-def _fill_site(site: NV.Site, ptr: int, vstride: int, cuts) -> None:
+def _fill_site(site: NV.Site, ptr: int, vstride: int, cuts, nvariants: int = 0) -> None:
     site.ptr = ptr
     site.sel = None
     site.zstride = 0
     site.vstride = vstride
+    site.nvariants = nvariants
     site.ncut = len(cuts)
     if len(cuts) > NV.MAX_CUTS:
         raise EngineError(f"{len(cuts)} cut legs on one site exceed TNC_MAX_CUTS")
@@ -358,7 +359,7 @@ class PathExecutor:
             d.dtype = self.code
             d.kernel = NV.K_AUTO
             dst, per_var, cuts = self.step_sites[i]
-            _fill_site(d.site, dst.data_ptr(), per_var, cuts)
+            _fill_site(d.site, dst.data_ptr(), per_var, cuts, self.nvar[sp.node])
             d.M, d.K, d.N = sp.M, sp.K, sp.N
             d.nf = len(sp.f_dim)
             for j in range(d.nf):
