@@ -88,7 +88,7 @@ typedef struct {
   tnc_site site;
   int64_t  M;
   int32_t  nf;
-  int32_t  _pad;
+  int32_t  c_n_contig;      /* 1 if c_noff[n] == n (rows may still be mapped) */
   int64_t  f_dim[TNC_MAX_LEGS];
   int64_t  f_astride[TNC_MAX_LEGS];
   int64_t  f_cstride[TNC_MAX_LEGS];

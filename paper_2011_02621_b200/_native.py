@@ -46,7 +46,7 @@ class StepDesc(C.Structure):
         ("dtype", C.c_int32), ("kernel", C.c_int32), ("Z", C.c_int64), ("slices_per_b", C.c_int64),
         ("s0", C.c_int64), ("acc", C.c_void_p), ("acc_zstride", C.c_int64),
         ("out", C.c_void_p), ("out_zstride", C.c_int64), ("site", Site),
-        ("M", C.c_int64), ("nf", C.c_int32), ("_pad", C.c_int32),
+        ("M", C.c_int64), ("nf", C.c_int32), ("c_n_contig", C.c_int32),
         ("f_dim", C.c_int64 * MAX_LEGS), ("f_astride", C.c_int64 * MAX_LEGS),
         ("f_cstride", C.c_int64 * MAX_LEGS), ("K", C.c_int64), ("N", C.c_int64),
         ("a_koff", C.c_void_p), ("b_koff", C.c_void_p), ("b_noff", C.c_void_p), ("c_noff", C.c_void_p),

@@ -294,7 +294,8 @@ k_pair_pipe(const __grid_constant__ PairTile p, const void* __restrict__ A_, con
         }
       }
     }
-    __syncthreads();   // everyone is done with this stage
+    fence_proxy_async();   // order this stage's generic reads before the async-proxy refill
+    __syncthreads();       // everyone is done with this stage
     if (threadIdx.x == 0 && t + PIPE_STAGES < t1)
       issue_tile<C>(p, A, t + PIPE_STAGES, ring + stage * tile_elems, &bars[stage]);
   }
@@ -370,6 +371,7 @@ k_pair_pipe_cols(const __grid_constant__ PairTile p, const void* __restrict__ A_
         if (k < K) cfma(acc, trow[koff_s[k]], scol[k]);
       Ot[(int64_t)row * N + n] = acc;
     }
+    fence_proxy_async();
     __syncthreads();
     if (threadIdx.x == 0 && t + PIPE_STAGES < t1)
       issue_tile<C>(p, A, t + PIPE_STAGES, ring + stage * tile_elems, &bars[stage]);

@@ -111,7 +111,6 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
@@ -343,7 +342,6 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
           const int32_t* kr = kraw_s + c * KC;
 #pragma unroll
           for (int q = 0; q < KC; ++q) v[q] = raw[kr[q]];
-          if (c == nchunk - 1) mbar_arrive_warp(&rempty[t % RS]);   // this tile's raw values are in registers
         } else {
           const int64_t* ko = akoff_s + c * KC;
 #pragma unroll
@@ -373,6 +371,12 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
         if (!(p.dbg & 512)) tmem_wait_st();
         tc_fence_before();
         mbar_arrive_warp(&full[stage]);
+        if (RS > 0 && c == nchunk - 1) {
+          // the tile's raw values have been consumed (converted and stored);
+          // order these generic reads before the async-proxy refill
+          fence_proxy_async();
+          mbar_arrive_warp(&rempty[t % RS]);
+        }
         if ((warp & 3) == 0 && c == nchunk - 1) TC_TRACE(2, t);
       }
     }

@@ -1,18 +1,32 @@
 // Tensor-core GEMM path for large engine steps (complex64): C[z] = A[z] S(z)
 // with A row-contiguous [M][K] (the engine's due-ordered accumulator), K a
-// multiple of 16 (or 4 / 8), any N (tiled by NT <= 64 complex) and a general
-// result map out = rowC(f) + c_noff[n] (the due-ordered result layout).
+// multiple of 8, any N (tiled by NT <= 64 complex) and a general result map
+// out = rowC(f) + c_noff[n] (the due-ordered result layout).
 //
-// Differences from k_tc_c64 (the skinny / sweep kernel): the site operand is
-// not resident -- B' (complex->real embedding, tf32 hi/lo, canonical K-major
-// chunks) is prepared once per distinct site block ("combo" = projected
-// variant x slice digits of this node's cut legs) by k_bprime and streamed per
-// K chunk by a cp.async.bulk producer; work items are (z, 128-row tile, N tile)
-// with the N tiles of a row tile consecutive, so the A tile is re-read from L2.
+// The complex product runs on de-interleaved operands as two real products of
+// width N = 2*NT into one accumulator D = [D_re | D_im]:
+//   D += Ar [Br | Bi],   D += Ai [-Bi | Br],
+// both windows of the three smem blocks [-Bi | Br | Bi] (3/4 of the bytes of
+// the 2x2 real embedding, and MMAs of N = 128 -- the full-rate width; N = 64
+// MMAs issue ~30% slower).  Each real product is 3xTF32 (lo*hi + hi*lo +
+// hi*hi, fp32 accumulation in TMEM).
 //
-// Warps: 0-7 converters (2 groups alternate work items; global -> tf32 hi/lo ->
-// TMEM), 8-11 epilogue, 12 MMA issuer, 13 B' producer.
+// Data movement:
+//  * A tiles (128 rows x KC complex) arrive by TMA (cp.async.bulk.tensor.3d,
+//    128B/64B swizzle) in a raw smem ring; converter warps read them
+//    conflict-free, split to tf32 hi/lo, de-interleave re/im and write the A
+//    operand into TMEM (tcgen05.st).  Rows past M are zero-filled by TMA.
+//  * Br/Bi hi/lo chunks (canonical K-major, prepared per call per distinct
+//    site block by k_bprime) stream in by cp.async.bulk.
+//  * Epilogue: tcgen05.ld of D_re / D_im -> complex; when the innermost
+//    result leg is a new leg the tile is staged in padded smem and written
+//    n-major with 16-byte stores, otherwise (innermost leg is a free leg)
+//    per-row stores, which are then coalesced across lanes.
+//
+// Warps: 0-7 converters (each chunk: 4 lane quadrants x 2 K halves), 8-11 epilogue,
+// 12 MMA issuer, 13 A producer (TMA), 14 B producer (bulk copies).
 #pragma once
+#include <cuda.h>
 #include "tnc_tc.cuh"
 
 namespace tnc {
@@ -20,16 +34,16 @@ namespace tnc {
 struct GemmDesc {
   int64_t Z, M, K, N;
   int64_t tiles_m, per_cta, items;
-  int32_t NT, tiles_n;           // complex columns per N tile
+  int32_t NT, tiles_n;           // complex columns per N tile (multiple of 16)
   int32_t KC, nchunk;            // complex K per chunk
-  const float2* a;
-  int64_t a_zstride;
-  const float* bp;               // [combo][tile_n][chunk][hi|lo][2NT x 2KC] canonical
+  int32_t RS, BS;                // raw A stages, B stages
+  int32_t dbg, _pad0;            // TNC_TG_DEBUG: 1 = MMA-only timing (no operand waits)
+  const float* bp;               // [combo][tile_n][chunk][hi: -Bi|Br|Bi][lo: -Bi|Br|Bi][NT x KC] canonical
   int64_t bp_combo_stride;       // floats per combo
   tnc_site site;                 // site blocks: combo -> offset
   const int64_t* b_koff;         // [K] site offsets
   const int64_t* b_noff;         // [N]
-  int32_t conj_b, _pad;
+  int32_t conj_b, n_contig;      // n_contig: c_noff[n] == n
   int64_t slices_per_b, s0;
   float2* out;
   int64_t out_zstride;
@@ -38,9 +52,10 @@ struct GemmDesc {
   const int64_t* c_noff;         // [N]
 };
 
-constexpr int TG_THREADS = 14 * 32;
-constexpr int TG_MMA_WARP = 12, TG_PROD_WARP = 13;
-constexpr int TG_BSTAGES = 4;
+constexpr int TG_THREADS = 15 * 32;
+constexpr int TG_EPI_WARP0 = 8, TG_MMA_WARP = 12, TG_APROD_WARP = 13, TG_BPROD_WARP = 14;
+constexpr int TG_MAX_RS = 8, TG_MAX_BS = 8;
+constexpr int TG_EPI_PITCH = 16 * 8 + 16;      // staged row: 16 complex + 16 B pad
 
 __device__ __forceinline__ int64_t gemm_combo(const GemmDesc& p, int64_t z) {
   const int64_t b = z / p.slices_per_b;
@@ -50,15 +65,17 @@ __device__ __forceinline__ int64_t gemm_combo(const GemmDesc& p, int64_t z) {
   return c;
 }
 
-__host__ __device__ inline int64_t tg_chunk_floats(int NT, int KC) { return (int64_t)(2 * NT) * (2 * KC); }
+__host__ __device__ inline int64_t tg_block_floats(int NT, int KC) { return (int64_t)NT * KC; }
 
-// B' for every (combo, N tile, K chunk): rows n' = 2n + c' of the tile, cols
-// k' = 2k + c of the chunk, K-major canonical (8 x 16 B core matrices, LBO =
-// 128 B along K, SBO = (2KC/4) * 128 B along N), hi chunk then lo chunk.
+// Site operand for every (combo, N tile, K chunk): hi then lo, each three
+// blocks [-Bi | Br | Bi] of NT rows (n) x KC cols (k), K-major canonical (8 x
+// 16 B core matrices, LBO = 128 B along K, SBO = (KC/4) * 128 B along N).
+// Consecutive blocks continue the 8-row-group sequence, so [Br | Bi] (blocks
+// 1-2) and [-Bi | Br] (blocks 0-1) are both one N = 2*NT descriptor.
 __global__ void k_bprime(const __grid_constant__ GemmDesc p, int64_t combos) {
-  const int NT = p.NT, KC = p.KC, KCr = 2 * KC;
-  const int64_t cf = tg_chunk_floats(NT, KC);
-  const uint32_t SBO = (KCr / 4) * 128;
+  const int NT = p.NT, KC = p.KC;
+  const int64_t bf = tg_block_floats(NT, KC);
+  const uint32_t SBO = (KC / 4) * 128;
   const int64_t per_combo = (int64_t)p.tiles_n * p.nchunk * NT * KC;
   const int64_t total = combos * per_combo;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
@@ -81,59 +98,72 @@ __global__ void k_bprime(const __grid_constant__ GemmDesc p, int64_t combos) {
       sv = reinterpret_cast<const float2*>(p.site.ptr)[off + p.b_koff[k] + p.b_noff[n]];
       if (p.conj_b) sv.y = -sv.y;
     }
-    float* base = const_cast<float*>(p.bp) + combo * p.bp_combo_stride + ((tn * p.nchunk + c) * 2) * cf;
-    const float vals[4] = {sv.x, -sv.y, sv.y, sv.x};
+    float* base = const_cast<float*>(p.bp) + combo * p.bp_combo_stride + ((tn * p.nchunk + c) * 6) * bf;
+    const uint32_t boff = (nl & 7) * 16 + (nl >> 3) * SBO + (kl >> 2) * 128 + (kl & 3) * 4;
+    float rh, rl, ih, il;
+    split3(sv.x, rh, rl);
+    split3(sv.y, ih, il);
+    const float v[6] = {-ih, rh, ih, -il, rl, il};
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int nr = 2 * nl + (q >> 1), kr = 2 * kl + (q & 1);
-      const uint32_t boff = (nr & 7) * 16 + (nr >> 3) * SBO + (kr >> 2) * 128 + (kr & 3) * 4;
-      float h, l;
-      split3(vals[q], h, l);
-      *reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(base) + boff) = h;
-      *reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(base + cf) + boff) = l;
-    }
+    for (int b = 0; b < 6; ++b) *reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(base + b * bf) + boff) = v[b];
   }
 }
 
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+
+
 template <int KC>
 __global__ void __launch_bounds__(TG_THREADS, 1)
-k_tc_gemm(const __grid_constant__ GemmDesc p) {
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
+k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMap tmA) {
+  extern __shared__ __align__(128) unsigned char smem_dyn[];
+  constexpr int RB = KC * 8;                       // raw row bytes (KC complex)
+  constexpr uint32_t SWM = RB == 128 ? 7u : 3u;    // swizzle row-group mask (128B / 64B)
+  constexpr uint32_t RAW_BYTES = 128 * RB;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int NT = p.NT, Nr = 2 * NT;
+  const int NT = p.NT;
   const int nchunk = p.nchunk;
-  const int64_t cf = tg_chunk_floats(NT, KC);
-  const uint32_t cbytes = (uint32_t)(cf * 4);
-  const uint32_t SBO_B = ((2 * KC) / 4) * 128;
-  // TMEM: 2 accumulators of Nr columns, A stages of 4*KC columns (hi + lo)
-  const int TS = 2;
+  const int RS = p.RS, BS = p.BS;
+  const int64_t bf = tg_block_floats(NT, KC);
+  const uint32_t bbytes = (uint32_t)(bf * 4);      // one block (NT x KC floats)
+  const uint32_t SBO_B = (KC / 4) * 128;
+  // TMEM: TS accumulators of [D_re NT | D_im NT], A stages of 4*KC columns
+  constexpr int TS = 2;
   constexpr uint32_t ACOLS = 4 * KC;
-  const int AS = min(TC_MAX_STAGES, (512 - TS * Nr) / (int)ACOLS) & ~1;   // even: 2 converter groups
-  const int ASg = AS / 2;
-  const uint32_t A0 = (uint32_t)(TS * Nr);
-  // smem: B ring [TG_BSTAGES][hi|lo chunk], c_noff tile, barriers
-  unsigned char* bring = smem_raw;
-  int64_t* cno = reinterpret_cast<int64_t*>(bring + (size_t)TG_BSTAGES * 2 * cbytes);   // [NT]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(cno + 64);
-  uint64_t* afull = bar;                         // [AS]
-  uint64_t* aempty = bar + TC_MAX_STAGES;        // [AS]
-  uint64_t* bfull = bar + 2 * TC_MAX_STAGES;     // [TG_BSTAGES]
-  uint64_t* bempty = bfull + TG_BSTAGES;         // [TG_BSTAGES]
-  uint64_t* tfull = bempty + TG_BSTAGES;         // [TS]
-  uint64_t* tempty = tfull + 2;                  // [TS]
+  const int AS = min(TC_MAX_STAGES, (512 - TS * 2 * NT) / (int)ACOLS);
+  const uint32_t A0 = (uint32_t)(TS * 2 * NT);
+  // smem: raw A ring (1024-aligned stages: swizzle atoms), B ring, epilogue staging, barriers
+  unsigned char* araw = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
+  unsigned char* bring = araw + (size_t)RS * RAW_BYTES;
+  unsigned char* estage = bring + (size_t)BS * 6 * bbytes;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(estage + 4 * 32 * TG_EPI_PITCH);
+  uint64_t* rfull = bar;                           // [RS] TMA -> converters
+  uint64_t* rempty = rfull + TG_MAX_RS;            // [RS] converters -> TMA
+  uint64_t* afull = rempty + TG_MAX_RS;            // [AS] converters -> MMA
+  uint64_t* aempty = afull + TC_MAX_STAGES;        // [AS] MMA -> converters
+  uint64_t* bfull = aempty + TC_MAX_STAGES;        // [BS]
+  uint64_t* bempty = bfull + TG_MAX_BS;            // [BS]
+  uint64_t* tfull = bempty + TG_MAX_BS;            // [TS]
+  uint64_t* tempty = tfull + 2;                    // [TS]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int64_t w0 = blockIdx.x * p.per_cta;
   const int64_t w1 = min(w0 + p.per_cta, p.items);
   const int nitems = (int)(w1 - w0);
+  const int64_t per_z = p.tiles_m * p.tiles_n;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < AS; ++s) { mbar_init(&afull[s], 4); mbar_init(&aempty[s], 1); }
-    for (int s = 0; s < TG_BSTAGES; ++s) { mbar_init(&bfull[s], 1); mbar_init(&bempty[s], 1); }
+    for (int s = 0; s < RS; ++s) { mbar_init(&rfull[s], 1); mbar_init(&rempty[s], 8); }
+    for (int s = 0; s < AS; ++s) { mbar_init(&afull[s], 8); mbar_init(&aempty[s], 1); }
+    for (int s = 0; s < BS; ++s) { mbar_init(&bfull[s], 1); mbar_init(&bempty[s], 1); }
     for (int s = 0; s < TS; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 4); }
     mbar_fence_init();
   }
-  if (warp == 8) {
+  if (warp == TG_EPI_WARP0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
@@ -141,65 +171,64 @@ k_tc_gemm(const __grid_constant__ GemmDesc p) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int64_t per_z = p.tiles_m * p.tiles_n;
 
-  if (warp < 8) {
-    // ---------------- converters ----------------
-    const int grp = warp >> 2;
+  if (warp < 8 && !(p.dbg & 1)) {
+    // ---------------- converters: raw smem -> tf32 hi/lo -> TMEM ----------------
+    // warp w converts rows 32*(w%4).. (its TMEM lane quadrant), complex
+    // [h*KC/2, (h+1)*KC/2) with h = w/4; all 8 warps work on every chunk.
+    const int h = warp >> 2;
     const int r = (warp & 3) * 32 + lane;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    constexpr int KH = KC / 2;                     // complex per warp
     int j = 0;
-    for (int it = grp; it < nitems; it += 2) {
-      const int64_t w = w0 + it;
-      const int64_t z = w / per_z;
-      const int64_t rem = w - z * per_z;
-      const int64_t mt = rem / p.tiles_n;
-      const int64_t row = mt * 128 + r;
-      const bool valid = row < p.M;
-      const float2* Ar = p.a + z * p.a_zstride + (valid ? row : 0) * p.K;
-      float2 v[KC];
-      auto ld = [&](int c) {
-#pragma unroll
-        for (int q = 0; q < KC; q += 2) {
-          if (valid) {
-            const float4 x = __ldg(reinterpret_cast<const float4*>(Ar + c * KC + q));
-            v[q] = make_float2(x.x, x.y);
-            v[q + 1] = make_float2(x.z, x.w);
-          } else {
-            v[q] = v[q + 1] = make_float2(0.f, 0.f);
-          }
-        }
-      };
-      ld(0);
+    for (int it = 0; it < nitems; ++it) {
       for (int c = 0; c < nchunk; ++c, ++j) {
-        const int stage = grp * ASg + j % ASg;
-        const uint32_t ph = (j / ASg) & 1;
-        uint32_t hi[2 * KC], lo[2 * KC];
+        const int rstage = j % RS;
+        const int astage = j % AS;
+        mbar_wait_spin(&rfull[rstage], (j / RS) & 1);
+        const uint32_t src = smem_u32(araw + (size_t)rstage * RAW_BYTES);
+        uint32_t rh[KH], ih[KH], rl[KH], il[KH];
 #pragma unroll
-        for (int q = 0; q < KC; ++q) {
-          float a, b;
-          split3(v[q].x, a, b);
-          hi[2 * q] = __float_as_uint(a);
-          lo[2 * q] = __float_as_uint(b);
-          split3(v[q].y, a, b);
-          hi[2 * q + 1] = __float_as_uint(a);
-          lo[2 * q + 1] = __float_as_uint(b);
+        for (int q = 0; q < KH / 2; ++q) {         // 16-byte piece: complex 2q, 2q+1 of this half
+          const uint32_t off = (uint32_t)(r * RB + 16 * (h * KH / 2 + q));
+          const uint32_t phys = off ^ (((off >> 7) & SWM) << 4);
+          float4 x;
+          asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w) : "r"(src + phys));
+          float hh, ll;
+          split3(x.x, hh, ll); rh[2 * q] = __float_as_uint(hh);     rl[2 * q] = __float_as_uint(ll);
+          split3(x.y, hh, ll); ih[2 * q] = __float_as_uint(hh);     il[2 * q] = __float_as_uint(ll);
+          split3(x.z, hh, ll); rh[2 * q + 1] = __float_as_uint(hh); rl[2 * q + 1] = __float_as_uint(ll);
+          split3(x.w, hh, ll); ih[2 * q + 1] = __float_as_uint(hh); il[2 * q + 1] = __float_as_uint(ll);
         }
-        if (c + 1 < nchunk) ld(c + 1);             // next chunk's loads in flight during the handoff
-        mbar_wait(&aempty[stage], ph ^ 1);
+        mbar_wait_spin(&aempty[astage], ((j / AS) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t col = A0 + (uint32_t)stage * ACOLS;
-        tmem_st<2 * KC>(tmem + lane_base + col, hi);
-        tmem_st<2 * KC>(tmem + lane_base + col + 2 * KC, lo);
+        // stage layout per 8-k step s: [Ar_hi 8 | Ai_hi 8 | Ar_lo 8 | Ai_lo 8]
+        const uint32_t k0 = (uint32_t)(h * KH);
+        const uint32_t col = A0 + (uint32_t)astage * ACOLS + (k0 / 8) * 32 + (k0 % 8);
+        tmem_st<KH>(tmem + lane_base + col, rh);
+        tmem_st<KH>(tmem + lane_base + col + 8, ih);
+        tmem_st<KH>(tmem + lane_base + col + 16, rl);
+        tmem_st<KH>(tmem + lane_base + col + 24, il);
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive_warp(&afull[stage]);
+        mbar_arrive_warp(&afull[astage]);
+        // release the raw stage only once its values have certainly been
+        // consumed (the shared loads can still be in flight when an earlier
+        // arrive retires, and the next TMA write would race them); the proxy
+        // fence orders these generic-proxy reads before the async-proxy refill
+        fence_proxy_async();
+        mbar_arrive_warp(&rempty[rstage]);
       }
     }
-  } else if (warp < 12) {
-    // ---------------- epilogue: TMEM -> registers -> result map ----------------
+  } else if (warp < TG_MMA_WARP) {
+    // ---------------- epilogue: TMEM -> complex -> result ----------------
     const int q = warp & 3;
     const int r = q * 32 + lane;
+    unsigned char* stg = estage + (size_t)q * 32 * TG_EPI_PITCH;
+    // staged n-major stores when the innermost result leg is a new leg (runs
+    // of consecutive n are contiguous); per-row stores otherwise (then the
+    // innermost result leg is a free leg: consecutive rows are contiguous)
+    const bool staged = p.c_rows_contig || p.n_contig || (p.N > 1 && p.c_noff[1] == p.c_noff[0] + 1);
     for (int it = 0; it < nitems; ++it) {
       const int acc = it % TS;
       const uint32_t ph = (it / TS) & 1;
@@ -208,7 +237,6 @@ k_tc_gemm(const __grid_constant__ GemmDesc p) {
       const int64_t rem = w - z * per_z;
       const int64_t mt = rem / p.tiles_n, nt = rem - mt * p.tiles_n;
       const int64_t row = mt * 128 + r;
-      // row map (mixed radix over the free legs) while the MMAs run
       int64_t oc = row * p.N;
       if (!p.c_rows_contig && row < p.M) {
         int64_t f = row;
@@ -223,29 +251,56 @@ k_tc_gemm(const __grid_constant__ GemmDesc p) {
       const int64_t n0 = nt * NT;
       mbar_wait(&tfull[acc], ph);
       tc_fence_after();
-      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * Nr);
-      for (int c0 = 0; c0 < Nr; c0 += 32) {
-        uint32_t vv[32];
-        if (c0 + 32 <= Nr) {
-          tmem_ld32(taddr + c0, vv);
-        } else {
-          uint32_t w16[16];
-          tmem_ld16(taddr + c0, w16);
-#pragma unroll
-          for (int jj = 0; jj < 16; ++jj) vv[jj] = w16[jj];
-        }
+      const uint32_t tre = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 2 * NT);
+      for (int c0 = 0; c0 < NT; c0 += 16) {
+        uint32_t vr[16], vi[16];
+        tmem_ld16(tre + c0, vr);
+        tmem_ld16(tre + NT + c0, vi);
         tmem_wait_ld();
-        if (c0 + 32 >= Nr) {
+        if (c0 + 16 >= NT) {
           tc_fence_before();
           mbar_arrive_warp(&tempty[acc]);
         }
-        if (row < p.M) {
+        const int64_t nleft = p.N - (n0 + c0);
+        const int ncols = nleft < 16 ? (int)nleft : 16;
+        if (staged) {
+          // stage the warp's 32 rows x 16 complex, then 8 lanes per row write
+          // 16-byte pieces: runs of consecutive n are contiguous in the result
+#pragma unroll
+          for (int jj = 0; jj < 16; jj += 2) {
+            const float4 v = make_float4(__uint_as_float(vr[jj]), __uint_as_float(vi[jj]),
+                                         __uint_as_float(vr[jj + 1]), __uint_as_float(vi[jj + 1]));
+            *reinterpret_cast<float4*>(stg + lane * TG_EPI_PITCH + jj * 8) = v;
+          }
+          __syncwarp();
+          const int sub = lane & 7;                // 16-byte piece (2 complex) of a row
+          const int64_t n = n0 + c0 + 2 * sub;
+          int64_t a0 = 0, a1 = 0;
+          if (2 * sub < ncols) a0 = p.c_rows_contig ? n : p.c_noff[n];
+          if (2 * sub + 1 < ncols) a1 = p.c_rows_contig ? n + 1 : p.c_noff[n + 1];
+#pragma unroll
+          for (int rr = 0; rr < 32; rr += 4) {
+            const int lr = rr + (lane >> 3);
+            const int64_t grow = mt * 128 + q * 32 + lr;
+            const int64_t ocr = __shfl_sync(0xffffffffu, oc, lr);
+            if (grow < p.M && 2 * sub < ncols) {
+              const float4 v = *reinterpret_cast<const float4*>(stg + lr * TG_EPI_PITCH + sub * 16);
+              float2* dst = O + ocr + a0;
+              if (2 * sub + 1 < ncols && a1 == a0 + 1 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+                *reinterpret_cast<float4*>(dst) = v;
+              } else {
+                dst[0] = make_float2(v.x, v.y);
+                if (2 * sub + 1 < ncols) O[ocr + a1] = make_float2(v.z, v.w);
+              }
+            }
+          }
+          __syncwarp();
+        } else if (row < p.M) {
 #pragma unroll
           for (int jj = 0; jj < 16; ++jj) {
-            const int64_t n = n0 + c0 / 2 + jj;
-            if (2 * jj < min(32, Nr - c0) && n < p.N) {
-              const float2 val = make_float2(__uint_as_float(vv[2 * jj]), __uint_as_float(vv[2 * jj + 1]));
-              O[p.c_rows_contig ? oc + n : oc + p.c_noff[n]] = val;
+            if (jj < ncols) {
+              const int64_t n = n0 + c0 + jj;
+              O[oc + p.c_noff[n]] = make_float2(__uint_as_float(vr[jj]), __uint_as_float(vi[jj]));
             }
           }
         }
@@ -253,32 +308,38 @@ k_tc_gemm(const __grid_constant__ GemmDesc p) {
     }
   } else if (warp == TG_MMA_WARP) {
     // ---------------- MMA issuer ----------------
-    const uint32_t idesc = tf32_idesc(Nr);
+    const uint32_t idesc = tf32_idesc(2 * NT);
     int bi = 0;
     for (int it = 0; it < nitems; ++it) {
       const int acc = it % TS;
-      mbar_wait(&tempty[acc], ((it / TS) & 1) ^ 1);
+      mbar_wait_spin(&tempty[acc], ((it / TS) & 1) ^ 1);
       tc_fence_after();
-      const uint32_t d = tmem + (uint32_t)(acc * Nr);
-      const int g = it & 1;
+      const uint32_t dre = tmem + (uint32_t)(acc * 2 * NT);
       for (int c = 0; c < nchunk; ++c, ++bi) {
-        const int jj = (it >> 1) * nchunk + c;
-        const int stage = g * ASg + jj % ASg;
-        mbar_wait(&afull[stage], (jj / ASg) & 1);
-        const int bs = bi % TG_BSTAGES;
-        mbar_wait(&bfull[bs], (bi / TG_BSTAGES) & 1);
+        const int stage = bi % AS;
+        const int bs = bi % BS;
+        if (!(p.dbg & 1)) {
+          mbar_wait_spin(&afull[stage], (bi / AS) & 1);
+          mbar_wait_spin(&bfull[bs], (bi / BS) & 1);
+        }
         tc_fence_after();
         if (lane == 0) {
-          const uint32_t ahi = tmem + A0 + (uint32_t)stage * ACOLS, alo = ahi + 2 * KC;
-          const uint32_t bh = smem_u32(bring + (size_t)bs * 2 * cbytes);
-          const uint64_t dbh0 = umma_desc(bh, 128, SBO_B), dbl0 = umma_desc(bh + cbytes, 128, SBO_B);
+          const uint32_t b0 = smem_u32(bring + (size_t)bs * 6 * bbytes);
+          const uint64_t b2h = umma_desc(b0, 128, SBO_B), b1h = umma_desc(b0 + bbytes, 128, SBO_B);
+          const uint64_t b2l = umma_desc(b0 + 3 * bbytes, 128, SBO_B), b1l = umma_desc(b0 + 4 * bbytes, 128, SBO_B);
 #pragma unroll
-          for (int s = 0; s < KC / 4; ++s) {
-            const uint64_t step = (uint64_t)(s * 256) >> 4;
+          for (int s = 0; s < KC / 8; ++s) {
+            const uint64_t st = (uint64_t)(s * 256) >> 4;   // 8 k = 2 core matrices = 256 B
+            const uint32_t arh = tmem + A0 + (uint32_t)stage * ACOLS + 32 * s;
+            const uint32_t aih = arh + 8, arl = arh + 16, ail = arh + 24;
             const uint32_t first = (c == 0 && s == 0) ? 0u : 1u;
-            mma_tf32_ts(d, alo + 8 * s, dbh0 + step, idesc, first);
-            mma_tf32_ts(d, ahi + 8 * s, dbl0 + step, idesc, 1u);
-            mma_tf32_ts(d, ahi + 8 * s, dbh0 + step, idesc, 1u);
+            // small terms first (lo*hi, hi*lo), then hi*hi
+            mma_tf32_ts(dre, arl, b1h + st, idesc, first);
+            mma_tf32_ts(dre, ail, b2h + st, idesc, 1u);
+            mma_tf32_ts(dre, arh, b1l + st, idesc, 1u);
+            mma_tf32_ts(dre, aih, b2l + st, idesc, 1u);
+            mma_tf32_ts(dre, arh, b1h + st, idesc, 1u);
+            mma_tf32_ts(dre, aih, b2h + st, idesc, 1u);
           }
           umma_commit(&aempty[stage]);
           umma_commit(&bempty[bs]);
@@ -287,33 +348,66 @@ k_tc_gemm(const __grid_constant__ GemmDesc p) {
         __syncwarp();
       }
     }
-  } else if (warp == TG_PROD_WARP && lane == 0) {
-    // ---------------- B' producer ----------------
+  } else if (warp == TG_APROD_WARP && lane == 0 && !(p.dbg & 1)) {
+    // ---------------- A producer: TMA tiles into the group's raw slice ----------------
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+    int j = 0;
+    for (int it = 0; it < nitems; ++it) {
+      const int64_t w = w0 + it;
+      const int64_t z = w / per_z;
+      const int64_t mt = (w - z * per_z) / p.tiles_n;
+      for (int c = 0; c < nchunk; ++c, ++j) {
+        const int rs = j % RS;
+        mbar_wait_spin(&rempty[rs], ((j / RS) & 1) ^ 1);
+        mbar_expect_tx(&rfull[rs], RAW_BYTES);
+        tma_load_3d(araw + (size_t)rs * RAW_BYTES, &tmA, c * 2 * KC, (int)(mt * 128), (int)z, &rfull[rs]);
+      }
+    }
+  } else if (warp == TG_BPROD_WARP && lane == 0 && !(p.dbg & 1)) {
+    // ---------------- B producer: Br/Bi hi/lo chunks ----------------
     int bi = 0;
     for (int it = 0; it < nitems; ++it) {
       const int64_t w = w0 + it;
       const int64_t z = w / per_z;
       const int64_t nt = (w - z * per_z) % p.tiles_n;
-      const float* src = p.bp + gemm_combo(p, z) * p.bp_combo_stride + nt * nchunk * 2 * cf;
+      const float* src = p.bp + gemm_combo(p, z) * p.bp_combo_stride + nt * nchunk * 6 * bf;
       for (int c = 0; c < nchunk; ++c, ++bi) {
-        const int bs = bi % TG_BSTAGES;
-        mbar_wait(&bempty[bs], ((bi / TG_BSTAGES) & 1) ^ 1);
-        unsigned char* dst = bring + (size_t)bs * 2 * cbytes;
-        mbar_expect_tx(&bfull[bs], 2 * cbytes);
-        bulk_g2s(dst, src + c * 2 * cf, 2 * cbytes, &bfull[bs]);
+        const int bs = bi % BS;
+        mbar_wait_spin(&bempty[bs], ((bi / BS) & 1) ^ 1);
+        mbar_expect_tx(&bfull[bs], 6 * bbytes);
+        bulk_g2s(bring + (size_t)bs * 6 * bbytes, src + c * 6 * bf, 6 * bbytes, &bfull[bs]);
       }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 8) {
+  if (warp == TG_EPI_WARP0) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
 }
 
-__host__ inline size_t tg_smem_bytes(int NT, int KC) {
-  return (size_t)TG_BSTAGES * 2 * tg_chunk_floats(NT, KC) * 4 + 64 * 8 + 8 * TC_MAX_STAGES * 8 + 256;
+__host__ inline size_t tg_smem_bytes(int NT, int KC, int RS, int BS) {
+  return 1024 + (size_t)RS * 128 * KC * 8 + (size_t)BS * 6 * tg_block_floats(NT, KC) * 4 + 4 * 32 * TG_EPI_PITCH +
+         8 * (2 * TG_MAX_RS + 2 * TC_MAX_STAGES + 2 * TG_MAX_BS + 4) + 16;
+}
+
+typedef CUresult (*tg_encode_fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+inline tg_encode_fn tg_encoder() {
+  static tg_encode_fn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<tg_encode_fn>(f);
+  }
+  return fn;
 }
 
 // engine step on the GEMM path; returns 1 launched, 0 not applicable, -1 error
@@ -326,7 +420,6 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
     int KC;
     if (d.K % 16 == 0) KC = 16;
     else if (d.K == 8) KC = 8;
-    else if (d.K == 4) KC = 4;
     else return 0;
     int64_t combos = 1;
     if (d.site.sel) {
@@ -335,17 +428,18 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
     }
     for (int j = 0; j < d.site.ncut; ++j) combos *= d.site.cut_ext[j];
     if (d.site.zstride != 0 || combos > 4096 || d.nf > TNC_MAX_LEGS) return 0;
+    if ((((uintptr_t)d.acc) % 16) || (d.acc_zstride % 2)) return 0;
+    if (d.M > 0x7fffffffLL || d.Z > 0x7fffffffLL || 2 * d.K > 0x7fffffffLL) return 0;
+    tg_encode_fn enc = tg_encoder();
+    if (!enc) return 0;
     GemmDesc p;
     memset(&p, 0, sizeof p);
     p.Z = d.Z; p.M = d.M; p.K = d.K; p.N = d.N;
-    p.NT = d.N >= 64 ? 64 : (int)((d.N + 7) / 8 * 8);
+    p.NT = d.N >= 64 ? 64 : (int)((d.N + 15) / 16 * 16);
     p.tiles_n = (int)((d.N + p.NT - 1) / p.NT);
     p.KC = KC;
     p.nchunk = (int)(d.K / KC);
     p.tiles_m = (d.M + 127) / 128;
-    p.a = reinterpret_cast<const float2*>(d.acc);
-    p.a_zstride = d.acc_zstride;
-    if ((((uintptr_t)p.a) % 16) || (d.K % 2) || (d.acc_zstride % 2)) return 0;   // float4 row loads
     p.site = d.site;
     p.b_koff = d.b_koff; p.b_noff = d.b_noff;
     p.conj_b = d.conj_b;
@@ -356,8 +450,29 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
     p.c_rows_contig = d.c_rows_contig;
     for (int j = 0; j < d.nf; ++j) { p.f_dim[j] = d.f_dim[j]; p.f_cstride[j] = d.f_cstride[j]; }
     p.c_noff = d.c_noff;
-    const int64_t cf = tg_chunk_floats(p.NT, KC);
-    p.bp_combo_stride = (int64_t)p.tiles_n * p.nchunk * 2 * cf;
+    p.n_contig = (d.c_rows_contig || d.c_n_contig) ? 1 : 0;
+    if (const char* e = getenv("TNC_TG_DEBUG")) p.dbg = atoi(e);
+    // stages: fill the shared-memory budget
+    int RS = 4, BS = 3;
+    const size_t budget = 226 * 1024;
+    while (RS + 1 <= TG_MAX_RS && tg_smem_bytes(p.NT, KC, RS + 1, BS) <= budget) ++RS;
+    while (BS + 1 <= TG_MAX_BS && tg_smem_bytes(p.NT, KC, RS, BS + 1) <= budget) ++BS;
+    if (const char* e = getenv("TNC_TG_RS")) RS = atoi(e);
+    if (const char* e = getenv("TNC_TG_BS")) BS = atoi(e);
+    if (tg_smem_bytes(p.NT, KC, RS, BS) > budget) return 0;
+    p.RS = RS; p.BS = BS;
+    // A: [Z][M][2K floats] with row pitch K complex, batch pitch acc_zstride complex
+    CUtensorMap tm;
+    const cuuint64_t gdim[3] = {(cuuint64_t)(2 * d.K), (cuuint64_t)d.M, (cuuint64_t)d.Z};
+    const cuuint64_t gstr[2] = {(cuuint64_t)(d.K * 8), (cuuint64_t)(d.acc_zstride * 8)};
+    const cuuint32_t box[3] = {(cuuint32_t)(2 * KC), 128u, 1u};
+    const cuuint32_t estr[3] = {1u, 1u, 1u};
+    if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(d.acc), gdim, gstr, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, KC == 16 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return 0;
+    const int64_t bfl = tg_block_floats(p.NT, KC);
+    p.bp_combo_stride = (int64_t)p.tiles_n * p.nchunk * 6 * bfl;
     float* bp = nullptr;
     if (cudaMallocAsync(reinterpret_cast<void**>(&bp), (size_t)combos * p.bp_combo_stride * 4, s) != cudaSuccess) return -1;
     p.bp = bp;
@@ -372,17 +487,15 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
     p.items = p.Z * p.tiles_m * p.tiles_n;
     p.per_cta = (p.items + sms - 1) / sms;
     const int64_t grid = (p.items + p.per_cta - 1) / p.per_cta;
-    const size_t smem = tg_smem_bytes(p.NT, KC);
+    const size_t smem = tg_smem_bytes(p.NT, KC, RS, BS);
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_tc_gemm<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       cudaFuncSetAttribute(k_tc_gemm<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       cudaFuncSetAttribute(k_tc_gemm<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       attr = true;
     }
-    if (KC == 16) k_tc_gemm<16><<<(unsigned)grid, TG_THREADS, smem, s>>>(p);
-    else if (KC == 8) k_tc_gemm<8><<<(unsigned)grid, TG_THREADS, smem, s>>>(p);
-    else k_tc_gemm<4><<<(unsigned)grid, TG_THREADS, smem, s>>>(p);
+    if (KC == 16) k_tc_gemm<16><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm);
+    else k_tc_gemm<8><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm);
     const bool ok = cudaGetLastError() == cudaSuccess;
     cudaFreeAsync(bp, s);
     return ok ? 1 : -1;

@@ -374,6 +374,7 @@ class PathExecutor:
             d.c_noff = base + 16 * sp.K + 8 * sp.N
             d.a_rows_contig = 1
             d.c_rows_contig = 1 if sp.c_rows_contig else 0
+            d.c_n_contig = 1 if np.array_equal(sp.c_noff, np.arange(sp.N)) else 0
             d.b_dense = 1
             d.conj_b = 0
         pd.nsteps = len(plan.steps)
