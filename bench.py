@@ -17,6 +17,11 @@ Workloads (``--workload``):
   applies.
 * ``cfg0`` (configs[0]) -- full amplitudes: 3x3 lattice, 8 cycles, 64
   bitstrings, complex128, projected engine.  Unit: amplitudes/s.
+* ``syc53`` -- full amplitudes of the configs[4] circuit family (53-qubit
+  Sycamore lattice, ABCDCDAB, fSim(pi/2, pi/6)) at the deepest depth whose
+  unsliced projected network fits one B200 (8 cycles: 6.4e11 complex
+  multiplies and 2^29-element intermediates per amplitude), complex64,
+  bitstring batches of the executor's chunk size.  Unit: amplitudes/s.
 
 Timing: W warm-up steps, then K steps; every case (a timed iteration) is
 bracketed by CUDA events on the launching stream and preceded by an untimed
@@ -297,6 +302,160 @@ def sweep_e2e(args, cases, plans, inputs, dev, world):
             "steps": steps, "path": "PairPlan + project_variants on host-resident pinned buffers"}
 
 
+SYC_DEPTH = 8
+SYC_MAX_RANK = 12
+
+
+def syc_engine(dev, depth=SYC_DEPTH):
+    from paper_2011_02621_b200 import AmplitudeEngine, pattern_rqc, sycamore53_graph
+
+    graph, pats, _ = sycamore53_graph()
+    circ = pattern_rqc(graph, [pats[c] for c in "ABCDCDAB"], depth, seed=0)
+    return AmplitudeEngine(circ, dtype="complex64", max_rank=SYC_MAX_RANK, device=dev)
+
+
+def run_syc53(args, rank, world, dev):
+    """Amplitudes of the 53-qubit Sycamore circuit (projected engine): each
+    step evaluates one batch of B bitstrings (B = the executor's chunk, all
+    resident in HBM); each rank evaluates its own bitstrings (weak scaling)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2011_02621_b200 import _native as NV
+
+    hbm, bf16, peak_src = peaks()
+    t0 = time.perf_counter()
+    eng = syc_engine(dev)
+    setup_s = time.perf_counter() - t0
+    ex, plan = eng.executor, eng.plan
+    B = ex.max_z
+    rng = np.random.default_rng(100 + rank)
+    bits = rng.integers(0, 2, (B, 53)).astype(np.int32)
+    sel = eng.selectors(bits)
+    amp = torch.zeros(B, dtype=torch.complex64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        eng.amplitudes_device(sel, B, amp)
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    # each step's working set (2 x B x 4 GiB ping-pong buffers) is far larger than L2
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(dev.index) as clk:
+        for e0, e1 in evs:
+            e0.record(stream)
+            eng.amplitudes_device(sel, B, amp)
+            e1.record(stream)
+        torch.cuda.synchronize(dev)
+    t = sum(e0.elapsed_time(e1) for e0, e1 in evs) * 1e-3
+    barrier(world)
+    t_max = allreduce_max(t, world, dev)
+    value = world * B * args.steps / t_max
+    # per-step kernel times (untimed pass, one chunk): dominant kernel + path roofline
+    L = NV.lib()
+    sptr = C.c_void_p(stream.cuda_stream)
+    ex.run(sel, B, amp)
+    traffic = plan.step_traffic(8)
+    sev = [torch.cuda.Event(enable_timing=True) for _ in range(len(plan.steps) + 1)]
+    sev[0].record(stream)
+    for i in range(len(plan.steps)):
+        NV.check(L.tnc_step(C.byref(ex._steps[i]), sptr), "tnc_step")
+        sev[i + 1].record(stream)
+    torch.cuda.synchronize(dev)
+    tot_t = tot_roof = gemm_t = gemm_fl = 0.0
+    for i, sp in enumerate(plan.steps):
+        ts = sev[i].elapsed_time(sev[i + 1]) * 1e-3
+        by, fl = traffic[i][0] * B, traffic[i][1] * B
+        tot_t += ts
+        tot_roof += max(by / (hbm * 1e9), fl / (bf16 * 1e12))
+        if sp.K * sp.N >= 256 and sp.K % 8 == 0:      # tensor-core steps
+            gemm_t += ts
+            gemm_fl += fl
+    achieved = gemm_fl / gemm_t / 1e12 if gemm_t else 0.0
+    launches = ex.launches_per_chunk() + sum(1 for sp in plan.steps if sp.K * sp.N >= 256 and sp.K % 8 == 0)
+    res = {
+        "value": value, "unit": "amplitudes/s", "ms_per_step": 1e3 * t_max / args.steps,
+        "gpu_launches": launches * args.steps,
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
+                     "frac": achieved / bf16, "traffic": None,
+                     "peak_source": f"{peak_src} bf16_tflops (MEASURED_PEAKS.json); the kernel runs 3xTF32",
+                     "kernel": "tnc::k_tc_gemm (tcgen05 3xTF32 complex GEMM steps)",
+                     "algorithmic": "8*M*K*N flops per step per bitstring",
+                     "kernel_share_of_step": gemm_t / tot_t if tot_t else None,
+                     "path_roofline_frac": tot_roof / tot_t if tot_t else None,
+                     "path_roofline": "sum over steps of max(bytes/HBM, flops/bf16 peak) / sum of step times"},
+        "config": {"workload": "configs[4] circuit family: 53-qubit Sycamore, ABCDCDAB, "
+                               f"{SYC_DEPTH} cycles (deepest unsliced depth that fits one GPU)",
+                   "dtype": "complex64", "bitstrings_per_step": B, "max_rank": SYC_MAX_RANK,
+                   "multiplies_per_amplitude": plan.multiplies, "max_elems": plan.max_elems,
+                   "path_steps": len(plan.steps), "host_setup_s": setup_s,
+                   "l2": "inputs larger than L2 (2 x B x 4 GiB ping-pong buffers)"},
+        "clocks": clk.summary(), "dtype": "complex64",
+    }
+    if args.e2e:
+        outs = ["".join(map(str, row)) for row in bits]
+        eng.amplitudes(outs)
+        torch.cuda.synchronize(dev)
+        barrier(world)
+        steps = max(1, min(args.steps, 3))
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            eng.amplitudes(outs)
+        te = allreduce_max(time.perf_counter() - t0, world, dev)
+        res["e2e"] = {"value": world * B * steps / te, "unit": "amplitudes/s", "h2d_bytes_per_step": B * 53 * 4,
+                      "d2h_bytes_per_step": B * 8, "steps": steps,
+                      "path": "AmplitudeEngine.amplitudes(list of bitstring strings) -> host complex array"}
+    res["_plan_steps"] = [(sp.M, sp.K, sp.N) for sp in plan.steps]
+    return res
+
+
+def syc_plan_shapes_host(depth=SYC_DEPTH):
+    """(M, K, N) of every path step, computed on the host only (circuit, TNS
+    evolution, path search, plan) -- for the CPU reference arm."""
+    from paper_2011_02621_b200 import pattern_rqc, sycamore53_graph
+    from paper_2011_02621_b200 import network as NW
+    from paper_2011_02621_b200.circuit import fuse_single_qubit_gates
+    from paper_2011_02621_b200.engine import ContractionPlan, NetworkSpec
+    from paper_2011_02621_b200.tns import evolve, init_state
+
+    graph, pats, _ = sycamore53_graph()
+    circ = pattern_rqc(graph, [pats[c] for c in "ABCDCDAB"], depth, seed=0)
+    fused = fuse_single_qubit_gates(circ)
+    phi = evolve(init_state(fused.graph, "0" * 53), fused, range(fused.depth), "forward", 1e-12)
+    edges = {e: phi.bond_dims[e] for e in fused.graph.edges}
+    path, _ = NW._path_for(NW._ShapeNet(range(53), edges), NW.CutPlan((), ()), SYC_MAX_RANK)
+    legs = {q: fused.graph.node_edges(q) for q in range(53)}
+    plan = ContractionPlan(NetworkSpec(list(range(53)), edges, legs), path)
+    return [(sp.M, sp.K, sp.N) for sp in plan.steps]
+
+
+def cpu_syc_rate(step_shapes, budget_s: float = 20.0):
+    """CPU time per amplitude for the syc53 path, estimated from the oracle's
+    contraction primitive (numpy tensordot, as tnsim.tensor.contract_pair) on
+    row samples of every distinct step shape (M_s = min(M, 2^14) rows of
+    [M, K] x [K, N], complex64), scaled by M / M_s."""
+    rng = np.random.default_rng(0)
+    shapes = sorted(set((K, N) for _, K, N in step_shapes), key=lambda x: -x[0] * x[1])
+    per_row = {}
+    t_start = time.perf_counter()
+    for K, N in shapes:
+        ms = 1 << 14
+        a = (rng.standard_normal((ms, K)) + 1j * rng.standard_normal((ms, K))).astype(np.complex64)
+        b = (rng.standard_normal((K, N)) + 1j * rng.standard_normal((K, N))).astype(np.complex64)
+        reps, t0 = 0, time.perf_counter()
+        while True:
+            np.tensordot(a, b, axes=([1], [0]))
+            reps += 1
+            if time.perf_counter() - t0 > min(1.0, budget_s / len(shapes)) or reps >= 20:
+                break
+        per_row[(K, N)] = (time.perf_counter() - t0) / reps / ms
+        if time.perf_counter() - t_start > budget_s:
+            break
+    worst = max(per_row.values())
+    t_amp = sum(M * per_row.get((K, N), worst) for M, K, N in step_shapes)
+    return 1.0 / t_amp, time.perf_counter() - t_start
+
+
 def run_cfg0(args, rank, world, dev):
     import torch
 
@@ -379,6 +538,15 @@ def cpu_sweep_rates(budget_s: float = 20.0):
     return rates, threads, time.perf_counter() - t_start
 
 
+def _cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+
+        return max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        return os.cpu_count() or 1
+
+
 def cpu_value_for(cases, rates):
     t = sum(case_traffic(*c)[0] / rates[(c[1], c[2])] for c in cases)
     return sum(c[3] for c in cases) / t
@@ -416,7 +584,7 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="sweep", choices=["sweep", "cfg0"])
+    ap.add_argument("--workload", default="sweep", choices=["sweep", "cfg0", "syc53"])
     ap.add_argument("--limit", type=int, default=SWEEP_LIMIT)
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu", dest="cpu", action="store_false")
@@ -428,6 +596,21 @@ def main():
     base = {"metric": METRIC, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "data": "synthetic (seeded)"}
 
+    if args.impl == "reference" and args.workload == "syc53":
+        if rank != 0:
+            return
+        shapes = syc_plan_shapes_host()
+        v, spent = cpu_syc_rate(shapes, args.cpu_budget)
+        line = dict(base, impl="reference", value=v, unit="amplitudes/s", n_gpus=world, dtype="complex64",
+                    ms_per_step=1e3 / v,
+                    config={"workload": "configs[4] circuit family: 53-qubit Sycamore, ABCDCDAB, "
+                                        f"{SYC_DEPTH} cycles", "dtype": "complex64"},
+                    cpu_baseline={"value": v, "unit": "amplitudes/s", "cores": _cpu_threads(), "kind": "port",
+                                  "sample": f"numpy tensordot on 2^14-row samples of every distinct step shape, "
+                                            f"{spent:.1f}s; scaled by rows"},
+                    e2e={"value": v, "unit": "amplitudes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
+        print(json.dumps(line))
+        return
     if args.impl == "reference":
         if rank != 0:
             return
@@ -454,7 +637,9 @@ def main():
     from paper_2011_02621_b200 import _native
 
     _native.require_device()
-    res = run_sweep(args, rank, world, dev) if args.workload == "sweep" else run_cfg0(args, rank, world, dev)
+    runner = {"sweep": run_sweep, "cfg0": run_cfg0, "syc53": run_syc53}[args.workload]
+    res = runner(args, rank, world, dev)
+    plan_steps = res.pop("_plan_steps", None)
     if rank == 0:
         if args.cpu and world == 1:
             if args.workload == "sweep":
@@ -463,6 +648,12 @@ def main():
                 res["cpu_baseline"] = {"value": cv, "unit": "bitstring-steps/s", "cores": threads, "kind": "port",
                                        "sample": f"oracle sweep_step (numpy) r=18, B=1 per (k,n), {spent:.1f}s; "
                                                  "scaled per case by algorithmic bytes"}
+            elif args.workload == "syc53" and plan_steps:
+                cv, spent = cpu_syc_rate(plan_steps, args.cpu_budget)
+                res["cpu_baseline"] = {"value": cv, "unit": "amplitudes/s", "cores": _cpu_threads(), "kind": "port",
+                                       "sample": f"numpy tensordot (the oracle/reference contraction primitive) on "
+                                                 f"2^14-row samples of every distinct step shape, {spent:.1f}s; "
+                                                 "scaled by rows (permutation cost not included: favours the CPU)"}
         detail = res.pop("detail", None)
         line = dict(base, **res)
         print(json.dumps(line))

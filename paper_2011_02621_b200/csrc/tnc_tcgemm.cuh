@@ -474,6 +474,22 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
     const int64_t bfl = tg_block_floats(p.NT, KC);
     p.bp_combo_stride = (int64_t)p.tiles_n * p.nchunk * 6 * bfl;
     float* bp = nullptr;
+    {
+      // keep freed stream-ordered blocks in the device pool across synchronizations
+      // (the default threshold returns them to the OS at every sync, and the next
+      // step's allocation would re-map memory)
+      static int pool_dev = -1;
+      int cur = 0;
+      cudaGetDevice(&cur);
+      if (pool_dev != cur) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, cur) == cudaSuccess) {
+          uint64_t thr = 1ull << 30;
+          cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        pool_dev = cur;
+      }
+    }
     if (cudaMallocAsync(reinterpret_cast<void**>(&bp), (size_t)combos * p.bp_combo_stride * 4, s) != cudaSuccess) return -1;
     p.bp = bp;
     {
