@@ -102,6 +102,13 @@ typedef struct {
   int32_t  c_rows_contig;   /* 1 if c_noff[n] == n and f_cstride.f == f*N   */
   int32_t  b_dense;         /* 1 if b_koff[k] == k*N and b_noff[n] == n      */
   int32_t  conj_b;          /* 1: contract with conj(site)                  */
+  /* Optional per-batch-element magnitude bounds (complex64; NULL = none):
+   * amax_out[z] <- max over out[z] of |re|, |im| (zeroed and written by the
+   * step), amax_in[z] = the same for acc[z] (the previous step's amax_out).
+   * With amax_in, tensor-core GEMM steps scale and split their operands into
+   * fp16 hi/lo pairs (two-fold MMA rate, same ~2^-22 product accuracy). */
+  float*       amax_out;
+  const float* amax_in;
 } tnc_step_desc;
 
 /* Gather: out[z][i] = site(z)[ sum_j digit_j(i) * src_stride[j] ], i mixed-radix

@@ -51,7 +51,7 @@ class StepDesc(C.Structure):
         ("f_cstride", C.c_int64 * MAX_LEGS), ("K", C.c_int64), ("N", C.c_int64),
         ("a_koff", C.c_void_p), ("b_koff", C.c_void_p), ("b_noff", C.c_void_p), ("c_noff", C.c_void_p),
         ("a_rows_contig", C.c_int32), ("c_rows_contig", C.c_int32), ("b_dense", C.c_int32),
-        ("conj_b", C.c_int32),
+        ("conj_b", C.c_int32), ("amax_out", C.c_void_p), ("amax_in", C.c_void_p),
     ]
 
 

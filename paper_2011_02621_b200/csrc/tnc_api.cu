@@ -110,18 +110,36 @@ void generic(const tnc_step_desc& d, cudaStream_t s) {
   tnc::k_step_generic<R, BM, BN, BK, TM, TN><<<(unsigned)(d.Z * tm * tn), (BM / TM) * (BN / TN), 0, s>>>(d, tm, tn);
 }
 
+// max |re|, |im| of out[z][0 .. M*N) for the kernels without a fused amax
+int launch_amax(const tnc_step_desc& d, cudaStream_t s) {
+  const int64_t count = d.M * d.N;
+  const int64_t zb = d.Z < 65535 ? d.Z : 65535;
+  int64_t bx = (count + 256 * 8 - 1) / (256 * 8);
+  const int64_t cap = std::max<int64_t>(1, 148 * 8 / zb);
+  if (bx > cap) bx = cap;
+  tnc::k_amax<<<dim3((unsigned)bx, (unsigned)zb), 256, 0, s>>>(reinterpret_cast<const float2*>(d.out), d.Z,
+                                                              d.out_zstride, count, d.amax_out);
+  return check_launch("tnc_step[amax]");
+}
+
 template <typename R>
-int launch_step(const tnc_step_desc& d, cudaStream_t s) {
-  if (d.Z <= 0 || d.M <= 0 || d.N <= 0) return TNC_OK;
-  if (d.K <= 0) return fail(TNC_E_INVALID, "tnc_step: K must be >= 1");
-  if (d.nf < 0 || d.nf > TNC_MAX_LEGS) return fail(TNC_E_INVALID, "tnc_step: nf=%d", d.nf);
-  if (d.site.ncut < 0 || d.site.ncut > TNC_MAX_CUTS) return fail(TNC_E_INVALID, "tnc_step: ncut=%d", d.site.ncut);
+int launch_step_kernel(const tnc_step_desc& d, cudaStream_t s, bool& fused_amax) {
   int kernel = d.kernel;
+  fused_amax = false;
   if (kernel == TNC_K_TC || (kernel == TNC_K_AUTO && tc_enabled())) {
     const int mask = kernel == TNC_K_TC ? 3 : tc_mask();
     int rc = 0;
-    if (mask & 1) rc = sizeof(R) == 8 ? tnc::try_dmma<R>(d, s) : tnc::try_tc<R>(d, s);
-    if (rc == 0 && (mask & 2) && sizeof(R) == 4) rc = tnc::try_tc_gemm<R>(d, s);
+    // with an input bound the fp16-split GEMM outruns the 3xTF32 resident kernel
+    const bool gemm_first = sizeof(R) == 4 && d.amax_in != nullptr && (mask & 2) && tnc::tc16_enabled();
+    if (gemm_first) {
+      rc = tnc::try_tc_gemm<R>(d, s);
+      if (rc == 1) fused_amax = true;
+    }
+    if (rc == 0 && (mask & 1)) rc = sizeof(R) == 8 ? tnc::try_dmma<R>(d, s) : tnc::try_tc<R>(d, s);
+    if (rc == 0 && !gemm_first && (mask & 2) && sizeof(R) == 4) {
+      rc = tnc::try_tc_gemm<R>(d, s);
+      if (rc == 1) fused_amax = true;
+    }
     if (rc == 1) return check_launch("tnc_step[tc]");
     if (rc < 0) return check_launch("tnc_step[tc] launch");
     if (kernel == TNC_K_TC) return fail(TNC_E_UNSUPPORTED, "tnc_step: shape outside the tensor-core kernel envelope");
@@ -134,6 +152,21 @@ int launch_step(const tnc_step_desc& d, cudaStream_t s) {
     return fail(TNC_E_INVALID, "tnc_step: generic kernel needs all four offset tables");
   generic<R>(d, s);
   return check_launch("tnc_step[generic]");
+}
+
+template <typename R>
+int launch_step(const tnc_step_desc& d, cudaStream_t s) {
+  if (d.Z <= 0 || d.M <= 0 || d.N <= 0) return TNC_OK;
+  if (d.K <= 0) return fail(TNC_E_INVALID, "tnc_step: K must be >= 1");
+  if (d.nf < 0 || d.nf > TNC_MAX_LEGS) return fail(TNC_E_INVALID, "tnc_step: nf=%d", d.nf);
+  if (d.site.ncut < 0 || d.site.ncut > TNC_MAX_CUTS) return fail(TNC_E_INVALID, "tnc_step: ncut=%d", d.site.ncut);
+  const bool want_amax = d.amax_out != nullptr && sizeof(R) == 4;
+  if (want_amax && cudaMemsetAsync(d.amax_out, 0, (size_t)d.Z * sizeof(float), s) != cudaSuccess)
+    return check_launch("tnc_step[amax zero]");
+  bool fused = false;
+  const int rc = launch_step_kernel<R>(d, s, fused);
+  if (rc != TNC_OK || !want_amax || fused) return rc;
+  return launch_amax(d, s);
 }
 
 template <typename R>
@@ -237,7 +270,7 @@ int launch_pair_tiled(const tnc::PairTile& p, int64_t batch, const void* a, cons
 
 extern "C" {
 
-int tnc_version(void) { return 100; }
+int tnc_version(void) { return 101; }
 
 size_t tnc_struct_size(int which) {
   switch (which) {

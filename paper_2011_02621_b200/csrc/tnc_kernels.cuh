@@ -251,5 +251,20 @@ k_slice_sum(const __grid_constant__ tnc_slice_sum_desc d) {
   }
 }
 
+// amax[z] = max |re|, |im| over x[z * zstride + i], i < count (atomicMax on
+// the float bits: non-negative floats order like their bit patterns)
+__global__ void k_amax(const float2* __restrict__ x, int64_t Z, int64_t zstride, int64_t count, float* amax) {
+  for (int64_t z = blockIdx.y; z < Z; z += gridDim.y) {
+    const float2* xz = x + z * zstride;
+    float m = 0.f;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+      const float2 v = __ldg(xz + i);
+      m = fmaxf(m, fmaxf(fabsf(v.x), fabsf(v.y)));
+    }
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(reinterpret_cast<unsigned int*>(amax) + z, __float_as_uint(m));
+  }
+}
+
 }  // namespace tnc
 

@@ -11,6 +11,15 @@
 // MMAs issue ~30% slower).  Each real product is 3xTF32 (lo*hi + hi*lo +
 // hi*hi, fp32 accumulation in TMEM).
 //
+// F16 mode (amax_in given): the same three products on fp16 operands, which
+// issue at twice the tf32 rate (kind::f16, K = 16 per MMA).  Every operand is
+// scaled by a power of two before the split -- A by 2^(15 - e(max|A[z]|))
+// from the producer's per-z amax, the site block by its own max -- so
+// |x| < 2^15, hi = fp16(x), lo = fp16(x - hi) carry 22 significant bits like
+// 3xTF32 (values below 2^-18 of the tensor max lose low bits of lo, which is
+// below the fp32 rounding of the tensor's L2 norm).  The epilogue undoes the
+// two scales exactly and, when asked, records max|out| per z for the next step.
+//
 // Data movement:
 //  * A tiles (128 rows x KC complex) arrive by TMA (cp.async.bulk.tensor.3d,
 //    128B/64B swizzle) in a raw smem ring; converter warps read them
@@ -27,6 +36,7 @@
 // 12 MMA issuer, 13 A producer (TMA), 14 B producer (bulk copies).
 #pragma once
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include "tnc_tc.cuh"
 
 namespace tnc {
@@ -37,9 +47,13 @@ struct GemmDesc {
   int32_t NT, tiles_n;           // complex columns per N tile (multiple of 16)
   int32_t KC, nchunk;            // complex K per chunk
   int32_t RS, BS;                // raw A stages, B stages
-  int32_t dbg, _pad0;            // TNC_TG_DEBUG: 1 = MMA-only timing (no operand waits)
-  const float* bp;               // [combo][tile_n][chunk][hi: -Bi|Br|Bi][lo: -Bi|Br|Bi][NT x KC] canonical
-  int64_t bp_combo_stride;       // floats per combo
+  int32_t dbg, _pad0;            // TNC_TG_DEBUG: 1 = MMA-only timing (no operand waits), 2 = no epilogue, 4 = epilogue without stores
+  const unsigned char* bp;       // [combo][tile_n][chunk][hi: -Bi|Br|Bi][lo: -Bi|Br|Bi][NT x KC] canonical
+  int64_t bp_combo_stride;       // bytes per combo
+  int32_t f16, cn_smem;          // 1: fp16 split operands (needs amax_in); c_noff staged in smem (int32)
+  const float* amax_in;          // [Z] max |re|,|im| of acc[z] (F16 scale)
+  float* amax_out;               // [Z] max |re|,|im| of out[z] (zeroed by the host), or null
+  const float* bscale;           // [combo] max |re|,|im| of the site block (F16)
   tnc_site site;                 // site blocks: combo -> offset
   const int64_t* b_koff;         // [K] site offsets
   const int64_t* b_noff;         // [N]
@@ -65,17 +79,72 @@ __device__ __forceinline__ int64_t gemm_combo(const GemmDesc& p, int64_t z) {
   return c;
 }
 
-__host__ __device__ inline int64_t tg_block_floats(int NT, int KC) { return (int64_t)NT * KC; }
+// bytes of one operand block (NT rows x KC k) -- fp32 or fp16 elements
+__host__ __device__ inline int64_t tg_block_bytes(int NT, int KC, int f16) { return (int64_t)NT * KC * (f16 ? 2 : 4); }
+
+// power-of-two scale s with max * s in [2^14, 2^15) (1 for a zero / non-finite max)
+__device__ __forceinline__ float f16_scale(float amax) {
+  if (!(amax > 0.f) || !(amax < 3.0e38f)) return 1.f;
+  const int e = (int)((__float_as_uint(amax) >> 23) & 0xff) - 127;   // amax in [2^e, 2^(e+1))
+  int p = 14 - e;
+  p = p < -126 ? -126 : (p > 127 ? 127 : p);
+  return __uint_as_float((uint32_t)(p + 127) << 23);
+}
+__device__ __forceinline__ void split_f16(float y, uint16_t& h, uint16_t& l) {
+  const __half hh = __float2half_rn(y);
+  const __half ll = __float2half_rn(y - __half2float(hh));
+  h = __half_as_ushort(hh);
+  l = __half_as_ushort(ll);
+}
+
+// Two values -> packed fp16 hi and lo (low half = y0).  hi is rounded to 11
+// significant bits in fp32 (integer add + mask, as split3) so lo = y - hi is
+// exact and each pair needs one packed conversion per part instead of a
+// round trip through fp16 per value.
+__device__ __forceinline__ void split_f16x2(float y0, float y1, uint32_t& h, uint32_t& l) {
+  const float h0 = __uint_as_float((__float_as_uint(y0) + 0x1000u) & 0xFFFFE000u);
+  const float h1 = __uint_as_float((__float_as_uint(y1) + 0x1000u) & 0xFFFFE000u);
+  const float l0 = y0 - h0, l1 = y1 - h1;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(h1), "f"(h0));
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(l) : "f"(l1), "f"(l0));
+}
+
+// per combo: max |re|, |im| over the site block (F16 scale of B')
+__global__ void k_bscale(const __grid_constant__ GemmDesc p, float* bscale) {
+  const int64_t combo = blockIdx.x;
+  int64_t off = 0, cc = combo;
+  for (int j = p.site.ncut - 1; j >= 0; --j) {
+    off += (cc % p.site.cut_ext[j]) * p.site.cut_stride[j];
+    cc /= p.site.cut_ext[j];
+  }
+  off += cc * p.site.vstride;
+  const float2* S = reinterpret_cast<const float2*>(p.site.ptr) + off;
+  float m = 0.f;
+  for (int64_t e = threadIdx.x; e < p.K * p.N; e += blockDim.x) {
+    const int64_t k = e / p.N, n = e - k * p.N;
+    const float2 v = S[p.b_koff[k] + p.b_noff[n]];
+    m = fmaxf(m, fmaxf(fabsf(v.x), fabsf(v.y)));
+  }
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ float red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, red[w]);
+    bscale[combo] = m;
+  }
+}
 
 // Site operand for every (combo, N tile, K chunk): hi then lo, each three
 // blocks [-Bi | Br | Bi] of NT rows (n) x KC cols (k), K-major canonical (8 x
 // 16 B core matrices, LBO = 128 B along K, SBO = (KC/4) * 128 B along N).
 // Consecutive blocks continue the 8-row-group sequence, so [Br | Bi] (blocks
 // 1-2) and [-Bi | Br] (blocks 0-1) are both one N = 2*NT descriptor.
+template <bool F16>
 __global__ void k_bprime(const __grid_constant__ GemmDesc p, int64_t combos) {
   const int NT = p.NT, KC = p.KC;
-  const int64_t bf = tg_block_floats(NT, KC);
-  const uint32_t SBO = (KC / 4) * 128;
+  const int64_t bbytes = tg_block_bytes(NT, KC, F16);
+  const uint32_t SBO = F16 ? (KC / 8) * 128 : (KC / 4) * 128;
   const int64_t per_combo = (int64_t)p.tiles_n * p.nchunk * NT * KC;
   const int64_t total = combos * per_combo;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
@@ -98,14 +167,25 @@ __global__ void k_bprime(const __grid_constant__ GemmDesc p, int64_t combos) {
       sv = reinterpret_cast<const float2*>(p.site.ptr)[off + p.b_koff[k] + p.b_noff[n]];
       if (p.conj_b) sv.y = -sv.y;
     }
-    float* base = const_cast<float*>(p.bp) + combo * p.bp_combo_stride + ((tn * p.nchunk + c) * 6) * bf;
-    const uint32_t boff = (nl & 7) * 16 + (nl >> 3) * SBO + (kl >> 2) * 128 + (kl & 3) * 4;
-    float rh, rl, ih, il;
-    split3(sv.x, rh, rl);
-    split3(sv.y, ih, il);
-    const float v[6] = {-ih, rh, ih, -il, rl, il};
+    unsigned char* base = const_cast<unsigned char*>(p.bp) + combo * p.bp_combo_stride + ((tn * p.nchunk + c) * 6) * bbytes;
+    if constexpr (F16) {
+      const uint32_t boff = (nl & 7) * 16 + (nl >> 3) * SBO + (kl >> 3) * 128 + (kl & 7) * 2;
+      const float t = f16_scale(p.bscale[combo]);
+      uint16_t rh, rl, ih, il;
+      split_f16(sv.x * t, rh, rl);
+      split_f16(sv.y * t, ih, il);
+      const uint16_t v[6] = {(uint16_t)(ih ^ 0x8000u), rh, ih, (uint16_t)(il ^ 0x8000u), rl, il};
 #pragma unroll
-    for (int b = 0; b < 6; ++b) *reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(base + b * bf) + boff) = v[b];
+      for (int b = 0; b < 6; ++b) *reinterpret_cast<uint16_t*>(base + b * bbytes + boff) = v[b];
+    } else {
+      const uint32_t boff = (nl & 7) * 16 + (nl >> 3) * SBO + (kl >> 2) * 128 + (kl & 3) * 4;
+      float rh, rl, ih, il;
+      split3(sv.x, rh, rl);
+      split3(sv.y, ih, il);
+      const float v[6] = {-ih, rh, ih, -il, rl, il};
+#pragma unroll
+      for (int b = 0; b < 6; ++b) *reinterpret_cast<float*>(base + b * bbytes + boff) = v[b];
+    }
   }
 }
 
@@ -117,9 +197,23 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
 }
 
 
-template <int KC>
+__device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
+      ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+// kind::f16 instruction descriptor: fp16 A/B (K-major), fp32 D, M = 128
+__device__ __forceinline__ uint32_t f16_idesc(int n_real) {
+  return (1u << 4) | ((uint32_t)(n_real >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
+template <int KC, bool F16>
 __global__ void __launch_bounds__(TG_THREADS, 1)
 k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMap tmA) {
+  static_assert(!F16 || KC == 16, "F16 mode needs 16-complex chunks (K = 16 per MMA)");
   extern __shared__ __align__(128) unsigned char smem_dyn[];
   constexpr int RB = KC * 8;                       // raw row bytes (KC complex)
   constexpr uint32_t SWM = RB == 128 ? 7u : 3u;    // swizzle row-group mask (128B / 64B)
@@ -128,28 +222,43 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
   const int NT = p.NT;
   const int nchunk = p.nchunk;
   const int RS = p.RS, BS = p.BS;
-  const int64_t bf = tg_block_floats(NT, KC);
-  const uint32_t bbytes = (uint32_t)(bf * 4);      // one block (NT x KC floats)
-  const uint32_t SBO_B = (KC / 4) * 128;
-  // TMEM: TS accumulators of [D_re NT | D_im NT], A stages of 4*KC columns
-  constexpr int TS = 2;
-  constexpr uint32_t ACOLS = 4 * KC;
+  const uint32_t bbytes = (uint32_t)tg_block_bytes(NT, KC, F16);   // one block (NT x KC)
+  const uint32_t SBO_B = F16 ? (KC / 8) * 128 : (KC / 4) * 128;
+  // TMEM: TS accumulators of [D_re NT | D_im NT], A stages of 4*KC (tf32) or
+  // 2*KC (fp16: two values per column) columns
+  constexpr uint32_t ACOLS = F16 ? 2 * KC : 4 * KC;
+  // warp roles: converters [0, CONVW), epilogue [CONVW, 12) in EPIG groups of
+  // four (one per TMEM lane quadrant; groups split the columns), 12 MMA, 13/14
+  // producers.  fp16 conversion is cheap, so F16 gives the epilogue 8 warps.
+  constexpr int CONVW = F16 ? 4 : 8;
+  constexpr int EPIW = TG_MMA_WARP - CONVW;
+  constexpr int EPIG = EPIW / 4;
+  // narrow tiles (NT <= 32, short epilogue per item, latency-bound): the
+  // epilogue groups alternate items instead of splitting columns, over four
+  // accumulator stages
+  const bool alt = F16 && NT <= 32;
+  const int TS = alt ? 4 : 2;
   const int AS = min(TC_MAX_STAGES, (512 - TS * 2 * NT) / (int)ACOLS);
   const uint32_t A0 = (uint32_t)(TS * 2 * NT);
   // smem: raw A ring (1024-aligned stages: swizzle atoms), B ring, epilogue staging, barriers
   unsigned char* araw = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
   unsigned char* bring = araw + (size_t)RS * RAW_BYTES;
   unsigned char* estage = bring + (size_t)BS * 6 * bbytes;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(estage + 4 * 32 * TG_EPI_PITCH);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(estage + EPIW * 32 * TG_EPI_PITCH);
   uint64_t* rfull = bar;                           // [RS] TMA -> converters
   uint64_t* rempty = rfull + TG_MAX_RS;            // [RS] converters -> TMA
   uint64_t* afull = rempty + TG_MAX_RS;            // [AS] converters -> MMA
   uint64_t* aempty = afull + TC_MAX_STAGES;        // [AS] MMA -> converters
   uint64_t* bfull = aempty + TC_MAX_STAGES;        // [BS]
   uint64_t* bempty = bfull + TG_MAX_BS;            // [BS]
-  uint64_t* tfull = bempty + TG_MAX_BS;            // [TS]
-  uint64_t* tempty = tfull + 2;                    // [TS]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tfull = bempty + TG_MAX_BS;            // [TS <= 4]
+  uint64_t* tempty = tfull + 4;                    // [TS <= 4]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 4);
+  // result column offsets (int32) staged once per CTA: the per-row epilogue
+  // reads one per value, and global loads there sit on its critical path
+  int32_t* cn_s = reinterpret_cast<int32_t*>(tmem_slot + 4);   // 16-byte aligned
+  if (p.cn_smem)
+    for (int n = threadIdx.x; n < p.N; n += blockDim.x) cn_s[n] = (int32_t)p.c_noff[n];
 
   const int64_t w0 = blockIdx.x * p.per_cta;
   const int64_t w1 = min(w0 + p.per_cta, p.items);
@@ -157,10 +266,10 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
   const int64_t per_z = p.tiles_m * p.tiles_n;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < RS; ++s) { mbar_init(&rfull[s], 1); mbar_init(&rempty[s], 8); }
-    for (int s = 0; s < AS; ++s) { mbar_init(&afull[s], 8); mbar_init(&aempty[s], 1); }
+    for (int s = 0; s < RS; ++s) { mbar_init(&rfull[s], 1); mbar_init(&rempty[s], CONVW); }
+    for (int s = 0; s < AS; ++s) { mbar_init(&afull[s], CONVW); mbar_init(&aempty[s], 1); }
     for (int s = 0; s < BS; ++s) { mbar_init(&bfull[s], 1); mbar_init(&bempty[s], 1); }
-    for (int s = 0; s < TS; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 4); }
+    for (int s = 0; s < TS; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], alt ? 4 : EPIW); }
     mbar_fence_init();
   }
   if (warp == TG_EPI_WARP0) {
@@ -172,21 +281,52 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp < 8 && !(p.dbg & 1)) {
-    // ---------------- converters: raw smem -> tf32 hi/lo -> TMEM ----------------
-    // warp w converts rows 32*(w%4).. (its TMEM lane quadrant), complex
-    // [h*KC/2, (h+1)*KC/2) with h = w/4; all 8 warps work on every chunk.
+  if (warp < CONVW && !(p.dbg & 1)) {
+    // ---------------- converters: raw smem -> tf32/fp16 hi/lo -> TMEM ----------------
+    // warp w converts rows 32*(w%4).. (its TMEM lane quadrant); tf32: complex
+    // [h*KC/2, (h+1)*KC/2) with h = w/4 (8 warps), F16: all KC complex (4 warps).
     const int h = warp >> 2;
     const int r = (warp & 3) * 32 + lane;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     constexpr int KH = KC / 2;                     // complex per warp
     int j = 0;
+    int rstage = 0, astage = 0;
+    uint32_t rph = 0, aph = 0;
     for (int it = 0; it < nitems; ++it) {
+      float sA = 1.f;
+      if constexpr (F16) sA = f16_scale(__ldg(p.amax_in + (w0 + it) / per_z));
       for (int c = 0; c < nchunk; ++c, ++j) {
-        const int rstage = j % RS;
-        const int astage = j % AS;
-        mbar_wait_spin(&rfull[rstage], (j / RS) & 1);
+        mbar_wait_spin(&rfull[rstage], rph);
         const uint32_t src = smem_u32(araw + (size_t)rstage * RAW_BYTES);
+        if constexpr (F16) {
+          // 16 complex -> 16 Ar and 16 Ai values, hi/lo fp16, two per TMEM column
+          uint32_t rh[KC / 2], ih[KC / 2], rl[KC / 2], il[KC / 2];
+#pragma unroll
+          for (int q = 0; q < KC / 2; ++q) {
+            const uint32_t off = (uint32_t)(r * RB + 16 * q);
+            const uint32_t phys = off ^ (((off >> 7) & SWM) << 4);
+            float4 x;
+            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w) : "r"(src + phys));
+            split_f16x2(x.x * sA, x.z * sA, rh[q], rl[q]);   // re of complex 2q, 2q+1
+            split_f16x2(x.y * sA, x.w * sA, ih[q], il[q]);   // im
+          }
+          mbar_wait_spin(&aempty[astage], aph ^ 1);
+          tc_fence_after();
+          // stage layout: [Ar_hi 8 | Ai_hi 8 | Ar_lo 8 | Ai_lo 8] columns (16 k each)
+          const uint32_t col = A0 + (uint32_t)astage * ACOLS;
+          tmem_st<KC / 2>(tmem + lane_base + col, rh);
+          tmem_st<KC / 2>(tmem + lane_base + col + 8, ih);
+          tmem_st<KC / 2>(tmem + lane_base + col + 16, rl);
+          tmem_st<KC / 2>(tmem + lane_base + col + 24, il);
+          tmem_wait_st();
+          tc_fence_before();
+          mbar_arrive_warp(&afull[astage]);
+          fence_proxy_async();
+          mbar_arrive_warp(&rempty[rstage]);
+          if (++rstage == RS) { rstage = 0; rph ^= 1; }
+          if (++astage == AS) { astage = 0; aph ^= 1; }
+          continue;
+        }
         uint32_t rh[KH], ih[KH], rl[KH], il[KH];
 #pragma unroll
         for (int q = 0; q < KH / 2; ++q) {         // 16-byte piece: complex 2q, 2q+1 of this half
@@ -200,7 +340,7 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
           split3(x.z, hh, ll); rh[2 * q + 1] = __float_as_uint(hh); rl[2 * q + 1] = __float_as_uint(ll);
           split3(x.w, hh, ll); ih[2 * q + 1] = __float_as_uint(hh); il[2 * q + 1] = __float_as_uint(ll);
         }
-        mbar_wait_spin(&aempty[astage], ((j / AS) & 1) ^ 1);
+        mbar_wait_spin(&aempty[astage], aph ^ 1);
         tc_fence_after();
         // stage layout per 8-k step s: [Ar_hi 8 | Ai_hi 8 | Ar_lo 8 | Ai_lo 8]
         const uint32_t k0 = (uint32_t)(h * KH);
@@ -218,18 +358,22 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
         // fence orders these generic-proxy reads before the async-proxy refill
         fence_proxy_async();
         mbar_arrive_warp(&rempty[rstage]);
+        if (++rstage == RS) { rstage = 0; rph ^= 1; }
+        if (++astage == AS) { astage = 0; aph ^= 1; }
       }
     }
   } else if (warp < TG_MMA_WARP) {
     // ---------------- epilogue: TMEM -> complex -> result ----------------
-    const int q = warp & 3;
+    const int q = warp & 3;                      // TMEM lane quadrant (CONVW is a multiple of 4)
+    const int eg = (warp - CONVW) >> 2;          // column group
     const int r = q * 32 + lane;
-    unsigned char* stg = estage + (size_t)q * 32 * TG_EPI_PITCH;
+    unsigned char* stg = estage + (size_t)(warp - CONVW) * 32 * TG_EPI_PITCH;
     // staged n-major stores when the innermost result leg is a new leg (runs
     // of consecutive n are contiguous); per-row stores otherwise (then the
     // innermost result leg is a free leg: consecutive rows are contiguous)
     const bool staged = p.c_rows_contig || p.n_contig || (p.N > 1 && p.c_noff[1] == p.c_noff[0] + 1);
-    for (int it = 0; it < nitems; ++it) {
+    const int cfirst = alt ? 0 : eg * 16, cstep = alt ? 16 : 16 * EPIG;
+    for (int it = alt ? eg : 0; it < nitems; it += alt ? EPIG : 1) {
       const int acc = it % TS;
       const uint32_t ph = (it / TS) & 1;
       const int64_t w = w0 + it;
@@ -249,18 +393,34 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
       }
       float2* O = p.out + z * p.out_zstride;
       const int64_t n0 = nt * NT;
+      float inv = 1.f, vmax = 0.f;
+      if constexpr (F16) inv = 1.f / (f16_scale(__ldg(p.amax_in + z)) * f16_scale(__ldg(p.bscale + gemm_combo(p, z))));
       mbar_wait(&tfull[acc], ph);
       tc_fence_after();
       const uint32_t tre = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 2 * NT);
-      for (int c0 = 0; c0 < NT; c0 += 16) {
+      if ((p.dbg & 2) || cfirst >= NT) {         // debug: drain nothing / no columns for this group
+        tc_fence_before();
+        mbar_arrive_warp(&tempty[acc]);
+        if (p.dbg & 2) continue;
+      }
+      float2* Orow = O + oc;
+      for (int c0 = cfirst; c0 < NT; c0 += cstep) {
         uint32_t vr[16], vi[16];
         tmem_ld16(tre + c0, vr);
         tmem_ld16(tre + NT + c0, vi);
         tmem_wait_ld();
-        if (c0 + 16 >= NT) {
+        if (c0 + cstep >= NT) {
           tc_fence_before();
           mbar_arrive_warp(&tempty[acc]);
         }
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          const float a = __uint_as_float(vr[jj]) * inv, b = __uint_as_float(vi[jj]) * inv;
+          vmax = fmaxf(vmax, fmaxf(fabsf(a), fabsf(b)));
+          vr[jj] = __float_as_uint(a);
+          vi[jj] = __float_as_uint(b);
+        }
+        if (p.dbg & 4) continue;                 // debug: TMEM loads only
         const int64_t nleft = p.N - (n0 + c0);
         const int ncols = nleft < 16 ? (int)nleft : 16;
         if (staged) {
@@ -276,8 +436,8 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
           const int sub = lane & 7;                // 16-byte piece (2 complex) of a row
           const int64_t n = n0 + c0 + 2 * sub;
           int64_t a0 = 0, a1 = 0;
-          if (2 * sub < ncols) a0 = p.c_rows_contig ? n : p.c_noff[n];
-          if (2 * sub + 1 < ncols) a1 = p.c_rows_contig ? n + 1 : p.c_noff[n + 1];
+          if (2 * sub < ncols) a0 = p.c_rows_contig ? n : (p.cn_smem ? cn_s[n] : p.c_noff[n]);
+          if (2 * sub + 1 < ncols) a1 = p.c_rows_contig ? n + 1 : (p.cn_smem ? cn_s[n + 1] : p.c_noff[n + 1]);
 #pragma unroll
           for (int rr = 0; rr < 32; rr += 4) {
             const int lr = rr + (lane >> 3);
@@ -296,19 +456,37 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
           }
           __syncwarp();
         } else if (row < p.M) {
+          if (p.cn_smem && ncols == 16) {
+            // 16 result offsets by four broadcast 16-byte shared loads; 32-bit indices
+            const int4* cq = reinterpret_cast<const int4*>(cn_s + n0 + c0);
+            int cidx[16];
 #pragma unroll
-          for (int jj = 0; jj < 16; ++jj) {
-            if (jj < ncols) {
-              const int64_t n = n0 + c0 + jj;
-              O[oc + p.c_noff[n]] = make_float2(__uint_as_float(vr[jj]), __uint_as_float(vi[jj]));
+            for (int u = 0; u < 4; ++u) {
+              const int4 t4 = cq[u];
+              cidx[4 * u] = t4.x; cidx[4 * u + 1] = t4.y; cidx[4 * u + 2] = t4.z; cidx[4 * u + 3] = t4.w;
+            }
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj)
+              Orow[cidx[jj]] = make_float2(__uint_as_float(vr[jj]), __uint_as_float(vi[jj]));
+          } else {
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) {
+              if (jj < ncols) {
+                const int64_t n = n0 + c0 + jj;
+                O[oc + (p.cn_smem ? (int64_t)cn_s[n] : p.c_noff[n])] = make_float2(__uint_as_float(vr[jj]), __uint_as_float(vi[jj]));
+              }
             }
           }
         }
       }
+      if (p.amax_out) {                          // rows past M / padded columns hold zeros
+        for (int o = 16; o; o >>= 1) vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+        if (lane == 0 && vmax > 0.f) atomicMax(reinterpret_cast<unsigned int*>(p.amax_out) + z, __float_as_uint(vmax));
+      }
     }
   } else if (warp == TG_MMA_WARP) {
     // ---------------- MMA issuer ----------------
-    const uint32_t idesc = tf32_idesc(2 * NT);
+    const uint32_t idesc = F16 ? f16_idesc(2 * NT) : tf32_idesc(2 * NT);
     int bi = 0;
     for (int it = 0; it < nitems; ++it) {
       const int acc = it % TS;
@@ -327,8 +505,19 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
           const uint32_t b0 = smem_u32(bring + (size_t)bs * 6 * bbytes);
           const uint64_t b2h = umma_desc(b0, 128, SBO_B), b1h = umma_desc(b0 + bbytes, 128, SBO_B);
           const uint64_t b2l = umma_desc(b0 + 3 * bbytes, 128, SBO_B), b1l = umma_desc(b0 + 4 * bbytes, 128, SBO_B);
+          if constexpr (F16) {
+            const uint32_t arh = tmem + A0 + (uint32_t)stage * ACOLS;
+            const uint32_t aih = arh + 8, arl = arh + 16, ail = arh + 24;
+            const uint32_t first = c == 0 ? 0u : 1u;
+            mma_f16_ts(dre, arl, b1h, idesc, first);
+            mma_f16_ts(dre, ail, b2h, idesc, 1u);
+            mma_f16_ts(dre, arh, b1l, idesc, 1u);
+            mma_f16_ts(dre, aih, b2l, idesc, 1u);
+            mma_f16_ts(dre, arh, b1h, idesc, 1u);
+            mma_f16_ts(dre, aih, b2h, idesc, 1u);
+          }
 #pragma unroll
-          for (int s = 0; s < KC / 8; ++s) {
+          for (int s = 0; s < (F16 ? 0 : KC / 8); ++s) {
             const uint64_t st = (uint64_t)(s * 256) >> 4;   // 8 k = 2 core matrices = 256 B
             const uint32_t arh = tmem + A0 + (uint32_t)stage * ACOLS + 32 * s;
             const uint32_t aih = arh + 8, arl = arh + 16, ail = arh + 24;
@@ -370,12 +559,12 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
       const int64_t w = w0 + it;
       const int64_t z = w / per_z;
       const int64_t nt = (w - z * per_z) % p.tiles_n;
-      const float* src = p.bp + gemm_combo(p, z) * p.bp_combo_stride + nt * nchunk * 6 * bf;
+      const unsigned char* src = p.bp + gemm_combo(p, z) * p.bp_combo_stride + (int64_t)nt * nchunk * 6 * bbytes;
       for (int c = 0; c < nchunk; ++c, ++bi) {
         const int bs = bi % BS;
         mbar_wait_spin(&bempty[bs], ((bi / BS) & 1) ^ 1);
         mbar_expect_tx(&bfull[bs], 6 * bbytes);
-        bulk_g2s(bring + (size_t)bs * 6 * bbytes, src + c * 6 * bf, 6 * bbytes, &bfull[bs]);
+        bulk_g2s(bring + (size_t)bs * 6 * bbytes, src + (int64_t)c * 6 * bbytes, 6 * bbytes, &bfull[bs]);
       }
     }
   }
@@ -387,9 +576,9 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
   }
 }
 
-__host__ inline size_t tg_smem_bytes(int NT, int KC, int RS, int BS) {
-  return 1024 + (size_t)RS * 128 * KC * 8 + (size_t)BS * 6 * tg_block_floats(NT, KC) * 4 + 4 * 32 * TG_EPI_PITCH +
-         8 * (2 * TG_MAX_RS + 2 * TC_MAX_STAGES + 2 * TG_MAX_BS + 4) + 16;
+__host__ inline size_t tg_smem_bytes(int NT, int KC, int RS, int BS, int f16, int64_t cn = 0) {
+  return 1024 + (size_t)RS * 128 * KC * 8 + (size_t)BS * 6 * tg_block_bytes(NT, KC, f16) + (f16 ? 8 : 4) * 32 * TG_EPI_PITCH +
+         8 * (2 * TG_MAX_RS + 2 * TC_MAX_STAGES + 2 * TG_MAX_BS + 8) + 16 + 4 * cn;
 }
 
 typedef CUresult (*tg_encode_fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -410,13 +599,25 @@ inline tg_encode_fn tg_encoder() {
   return fn;
 }
 
+// TNC_TC16=0 keeps complex64 GEMM steps on 3xTF32 even when amax_in is given
+inline bool tc16_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TNC_TC16");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v != 0;
+}
+
 // engine step on the GEMM path; returns 1 launched, 0 not applicable, -1 error
+// (when launched with amax_out set, the epilogue has recorded max |out| per z)
 template <typename R>
 int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
   if constexpr (sizeof(R) != 4) {
     return 0;
   } else {
     if (!d.a_rows_contig || d.K * d.N < 256) return 0;
+    if (d.Z * ((d.M + 127) / 128) < 64) return 0;     // too few row tiles to fill the GPU
     int KC;
     if (d.K % 16 == 0) KC = 16;
     else if (d.K == 8) KC = 8;
@@ -451,15 +652,28 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
     for (int j = 0; j < d.nf; ++j) { p.f_dim[j] = d.f_dim[j]; p.f_cstride[j] = d.f_cstride[j]; }
     p.c_noff = d.c_noff;
     p.n_contig = (d.c_rows_contig || d.c_n_contig) ? 1 : 0;
+    p.amax_out = d.amax_out;
+    const int f16 = (d.amax_in != nullptr && KC == 16 && tc16_enabled()) ? 1 : 0;
+    p.f16 = f16;
+    p.amax_in = f16 ? d.amax_in : nullptr;
+    if (const char* e = getenv("TNC_TG_NT")) {
+      const int nt = atoi(e);
+      if (nt >= 16 && nt % 16 == 0 && nt <= (f16 ? 96 : 64)) {
+        p.NT = nt;
+        p.tiles_n = (int)((d.N + p.NT - 1) / p.NT);
+      }
+    }
     if (const char* e = getenv("TNC_TG_DEBUG")) p.dbg = atoi(e);
     // stages: fill the shared-memory budget
     int RS = 4, BS = 3;
     const size_t budget = 226 * 1024;
-    while (RS + 1 <= TG_MAX_RS && tg_smem_bytes(p.NT, KC, RS + 1, BS) <= budget) ++RS;
-    while (BS + 1 <= TG_MAX_BS && tg_smem_bytes(p.NT, KC, RS, BS + 1) <= budget) ++BS;
+    p.cn_smem = (!d.c_rows_contig && d.N <= 1024 && d.out_zstride < 0x7fffffffLL) ? 1 : 0;
+    const int64_t cn = p.cn_smem ? d.N : 0;
+    while (RS + 1 <= TG_MAX_RS && tg_smem_bytes(p.NT, KC, RS + 1, BS, f16, cn) <= budget) ++RS;
+    while (BS + 1 <= TG_MAX_BS && tg_smem_bytes(p.NT, KC, RS, BS + 1, f16, cn) <= budget) ++BS;
     if (const char* e = getenv("TNC_TG_RS")) RS = atoi(e);
     if (const char* e = getenv("TNC_TG_BS")) BS = atoi(e);
-    if (tg_smem_bytes(p.NT, KC, RS, BS) > budget) return 0;
+    if (tg_smem_bytes(p.NT, KC, RS, BS, f16, cn) > budget) return 0;
     p.RS = RS; p.BS = BS;
     // A: [Z][M][2K floats] with row pitch K complex, batch pitch acc_zstride complex
     CUtensorMap tm;
@@ -471,9 +685,8 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
             CU_TENSOR_MAP_INTERLEAVE_NONE, KC == 16 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return 0;
-    const int64_t bfl = tg_block_floats(p.NT, KC);
-    p.bp_combo_stride = (int64_t)p.tiles_n * p.nchunk * 6 * bfl;
-    float* bp = nullptr;
+    p.bp_combo_stride = (int64_t)p.tiles_n * p.nchunk * 6 * tg_block_bytes(p.NT, KC, f16);
+    unsigned char* bp = nullptr;
     {
       // keep freed stream-ordered blocks in the device pool across synchronizations
       // (the default threshold returns them to the OS at every sync, and the next
@@ -490,12 +703,21 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
         pool_dev = cur;
       }
     }
-    if (cudaMallocAsync(reinterpret_cast<void**>(&bp), (size_t)combos * p.bp_combo_stride * 4, s) != cudaSuccess) return -1;
+    // one allocation: B' blocks, then (F16) the per-combo site maxima
+    const size_t bp_bytes = ((size_t)combos * p.bp_combo_stride + 255) & ~(size_t)255;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&bp), bp_bytes + (f16 ? combos * 4 : 0), s) != cudaSuccess) return -1;
     p.bp = bp;
     {
       const int64_t work = combos * p.tiles_n * p.nchunk * p.NT * KC;
       int blocks = (int)std::min<int64_t>((work + 255) / 256, 148 * 16);
-      k_bprime<<<blocks < 1 ? 1 : blocks, 256, 0, s>>>(p, combos);
+      if (f16) {
+        float* bsc = reinterpret_cast<float*>(bp + bp_bytes);
+        k_bscale<<<(unsigned)combos, 256, 0, s>>>(p, bsc);
+        p.bscale = bsc;
+        k_bprime<true><<<blocks < 1 ? 1 : blocks, 256, 0, s>>>(p, combos);
+      } else {
+        k_bprime<false><<<blocks < 1 ? 1 : blocks, 256, 0, s>>>(p, combos);
+      }
     }
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -503,15 +725,17 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
     p.items = p.Z * p.tiles_m * p.tiles_n;
     p.per_cta = (p.items + sms - 1) / sms;
     const int64_t grid = (p.items + p.per_cta - 1) / p.per_cta;
-    const size_t smem = tg_smem_bytes(p.NT, KC, RS, BS);
+    const size_t smem = tg_smem_bytes(p.NT, KC, RS, BS, f16, cn);
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_tc_gemm<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      cudaFuncSetAttribute(k_tc_gemm<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      cudaFuncSetAttribute(k_tc_gemm<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      cudaFuncSetAttribute(k_tc_gemm<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      cudaFuncSetAttribute(k_tc_gemm<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       attr = true;
     }
-    if (KC == 16) k_tc_gemm<16><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm);
-    else k_tc_gemm<8><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm);
+    if (f16) k_tc_gemm<16, true><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm);
+    else if (KC == 16) k_tc_gemm<16, false><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm);
+    else k_tc_gemm<8, false><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm);
     const bool ok = cudaGetLastError() == cudaSuccess;
     cudaFreeAsync(bp, s);
     return ok ? 1 : -1;

@@ -377,6 +377,18 @@ class PathExecutor:
             d.c_n_contig = 1 if np.array_equal(sp.c_noff, np.arange(sp.N)) else 0
             d.b_dense = 1
             d.conj_b = 0
+        # complex64 tensor-core GEMM steps take their input's per-z magnitude
+        # bound from the previous step (amax_out -> amax_in, two ping-pong
+        # rows), which lets them run fp16-split MMAs (tnc.h, tnc_tcgemm.cuh)
+        self._amax = None
+        if self.code == NV.C64 and len(plan.steps) > 1:
+            self._amax = self.torch.zeros((2, self.max_z), dtype=self.torch.float32, device=self.device)
+            for i in range(1, len(plan.steps)):
+                sp = plan.steps[i]
+                if sp.K % 16 == 0 and sp.K * sp.N >= 256:
+                    ptr = self._amax[i & 1].data_ptr()
+                    steps[i].amax_in = ptr
+                    steps[i - 1].amax_out = ptr
         pd.nsteps = len(plan.steps)
         pd.steps = C.cast(steps, C.POINTER(NV.StepDesc))
         pd.reduce.dtype = self.code

@@ -143,3 +143,51 @@ def test_tc_gemm_scaled_precision(M, K, N):
     ref = O.contract_along_path({q: (sites[q][0], legs[q]) for q in range(3)}, [0, 1, 2])[0]
     scale = O.contract_along_path({q: (np.abs(sites[q][0]), legs[q]) for q in range(3)}, [0, 1, 2])[0]
     assert abs(got - ref) / abs(scale) <= 2e-7
+
+
+@pytest.mark.parametrize("M,K,N,scale", [(8192, 128, 256, 1.0), (16384, 256, 128, 3e-21), (8192, 16, 128, 7e12),
+                                         (32768, 16, 16, 1.0), (8192, 64, 24, 1e-3)])
+def test_tc_gemm_f16_split_step(M, K, N, scale):
+    """fp16-split tcgen05 GEMM (a step given amax_in): one step acc[M, K] x
+    S[K, N] on inputs spanning ~12 decades around an arbitrary overall scale
+    matches the complex128 product to the 3xTF32 level (relative L2 <= 2e-6),
+    and amax_out records max |re|, |im| of the result."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2011_02621_b200 import _native as NV
+    from paper_2011_02621_b200.engine import ContractionPlan, NetworkSpec, PathExecutor
+
+    edges = {(0, 1): K, (0, 2): M, (1, 2): N}
+    legs = {0: [(0, 2), (0, 1)], 1: [(0, 1), (1, 2)], 2: [(0, 2), (1, 2)]}
+    spec = NetworkSpec([0, 1, 2], edges, legs)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(M + K + N)
+    sites = {q: torch.randn((1,) + spec.site_dims(q), dtype=torch.complex64, device="cuda", generator=g) for q in range(3)}
+    plan = ContractionPlan(spec, [0, 1, 2])
+    sp = plan.steps[0]
+    assert (sp.M, sp.K, sp.N) == (M, K, N)
+    ex = PathExecutor(plan, sites, dtype="complex64")
+    d = ex._steps[0]
+    Z = 2
+    mag = torch.exp(torch.empty(Z * M * K, device="cuda").uniform_(-14, 14, generator=g))
+    acc = (torch.randn(Z * M * K, dtype=torch.complex64, device="cuda", generator=g) * mag * scale).to(torch.complex64)
+    out = torch.zeros(Z * M * N, dtype=torch.complex64, device="cuda")
+    amax_in = torch.view_as_real(acc.reshape(Z, -1)).abs().reshape(Z, -1).amax(dim=1).contiguous()
+    amax_out = torch.zeros(Z, dtype=torch.float32, device="cuda")
+    d.Z, d.slices_per_b, d.s0 = Z, 1, 0
+    d.acc, d.acc_zstride = acc.data_ptr(), M * K
+    d.out, d.out_zstride = out.data_ptr(), M * N
+    d.site.sel = None
+    d.amax_in, d.amax_out = amax_in.data_ptr(), amax_out.data_ptr()
+    L = NV.lib()
+    NV.check(L.tnc_step(C.byref(d), C.c_void_p(torch.cuda.current_stream().cuda_stream)), "tnc_step")
+    torch.cuda.synchronize()
+    site = ex.step_sites[0][0][0].reshape(K, N).to(torch.complex128)
+    ref = acc.reshape(Z, M, K).to(torch.complex128) @ site
+    got = out.reshape(Z, M, N).to(torch.complex128)
+    err = ((got - ref).norm() / ref.norm()).item()
+    assert err <= 2e-6, err
+    want = torch.view_as_real(out.reshape(Z, -1)).abs().reshape(Z, -1).amax(dim=1)
+    assert torch.equal(amax_out, want), (amax_out, want)

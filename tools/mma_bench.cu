@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(128, 1) k_bench(int niter, unsigned long long*
   const uint32_t tmem = slot;
   if (threadIdx.x == 0) {
     uint32_t idesc;
-    if (MODE == 2) idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    if (MODE == 2 || MODE == 7) idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
     else idesc = tf32_idesc(N);
     const uint32_t b0 = smem_u32(sm);
     const uint64_t bd = umma_desc(b0, 128, 512);
@@ -43,6 +43,11 @@ __global__ void __launch_bounds__(128, 1) k_bench(int niter, unsigned long long*
       if (MODE == 0) mma_tf32_ts(tmem, tmem + 256, bd, idesc, acc);
       else if (MODE == 1) mma_tf32(tmem, ad, bd, idesc, acc);
       else if (MODE == 2) mma_f16_ts(tmem, tmem + 256, bd, idesc, acc);
+      else if (MODE == 7) {
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+                     ::"r"(tmem), "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+      }
       else if (MODE == 3) mma_tf32_ts(tmem + (i & 1) * N, tmem + 256 + 8 * (i & 3), bd, idesc, i < 2 ? 0u : 1u);
       else if (MODE >= 4) {
         // chunk-shaped: 12 MMAs per group of 12 iterations, commit(s) every 12
@@ -93,6 +98,9 @@ int main() {
   run<2, 64>("bf16 ts", 16);
   run<2, 128>("bf16 ts", 16);
   run<2, 256>("bf16 ts", 16);
+  run<7, 64>("bf16 ss", 16);
+  run<7, 128>("bf16 ss", 16);
+  run<7, 256>("bf16 ss", 16);
   run<3, 64>("tf32 ts 2acc", 8);
   run<3, 128>("tf32 ts 2acc", 8);
   run<4, 64>("tf32 ts chunk nocommit", 8);

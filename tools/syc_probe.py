@@ -48,6 +48,21 @@ def main():
     torch.cuda.synchronize()
     t_amp = e0.elapsed_time(e1) / reps * 1e-3
     print(f"B={B}: {t_amp * 1e3:.2f} ms per batch, {B / t_amp:.2f} amplitudes/s", flush=True)
+    if "--only" in sys.argv:               # one step inside an NVTX range (for ncu --nvtx-include probe/)
+        i = int(sys.argv[sys.argv.index("--only") + 1])
+        L = NV.lib()
+        sptr = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        ex.run(sel, ex.chunks(B, range(plan.slice_count))[0][1], amp)
+        for k in range(i):
+            NV.check(L.tnc_step(C.byref(ex._steps[k]), sptr), "tnc_step")
+        torch.cuda.synchronize()
+        torch.cuda.nvtx.range_push("probe")
+        NV.check(L.tnc_step(C.byref(ex._steps[i]), sptr), "tnc_step")
+        torch.cuda.nvtx.range_pop()
+        torch.cuda.synchronize()
+        sp = plan.steps[i]
+        print(f"ran step {i}: M={sp.M} K={sp.K} N={sp.N} contig={int(sp.c_rows_contig)}")
+        return
     # per-step timing (one chunk of the batch)
     L = NV.lib()
     st = torch.cuda.current_stream()
@@ -76,7 +91,7 @@ def main():
         rows.append({"i": i, "M": sp.M, "K": sp.K, "N": sp.N, "contig": bool(sp.c_rows_contig), "us": t * 1e6,
                      "GBps": by / t / 1e9, "TFs": fl / t / 1e12, "roof_us": roof * 1e6})
     rows.sort(key=lambda r: -r["us"])
-    for r in rows[:25]:
+    for r in (rows if "--all" in sys.argv else rows[:25]):
         print(f"step {r['i']:3d} M={r['M']:>10d} K={r['K']:>5d} N={r['N']:>5d} contig={int(r['contig'])} "
               f"{r['us']:10.1f} us {r['GBps']:8.1f} GB/s {r['TFs']:7.2f} TF/s roof {r['roof_us']:9.1f} us")
     print(f"z={z}: sum step time {tot_t * 1e3:.2f} ms, roofline {tot_roof * 1e3:.2f} ms, frac {tot_roof / tot_t:.3f}")
