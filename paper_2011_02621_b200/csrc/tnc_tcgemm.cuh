@@ -237,8 +237,13 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
   // epilogue groups alternate items instead of splitting columns, over four
   // accumulator stages
   const bool alt = F16 && NT <= 32;
-  const int TS = alt ? 4 : 2;
-  const int AS = min(TC_MAX_STAGES, (512 - TS * 2 * NT) / (int)ACOLS);
+  // NT = 128 (F16, one N tile for N = 128): a single accumulator stage
+  const int TS = alt ? 4 : (NT > 64 ? 1 : 2);
+  // A-resident (ares): the whole converted 128 x K tile fits TMEM next to the
+  // accumulators, so it is converted once per row tile and reused by all
+  // tiles_n column tiles (stage = chunk; released after the last column tile)
+  const bool ares = F16 && p.tiles_n > 1 && TS * 2 * NT + nchunk * (int)ACOLS <= 512 && nchunk <= TC_MAX_STAGES;
+  const int AS = ares ? nchunk : min(TC_MAX_STAGES, (512 - TS * 2 * NT) / (int)ACOLS);
   const uint32_t A0 = (uint32_t)(TS * 2 * NT);
   // smem: raw A ring (1024-aligned stages: swizzle atoms), B ring, epilogue staging, barriers
   unsigned char* araw = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
@@ -264,6 +269,9 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
   const int64_t w1 = min(w0 + p.per_cta, p.items);
   const int nitems = (int)(w1 - w0);
   const int64_t per_z = p.tiles_m * p.tiles_n;
+  // ares groups: consecutive items of one row tile (column tile index = w % tiles_n)
+  auto gstart = [&](int it) { return it == 0 || (w0 + it) % p.tiles_n == 0; };
+  auto gend = [&](int it) { return it == nitems - 1 || (w0 + it) % p.tiles_n == p.tiles_n - 1; };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < RS; ++s) { mbar_init(&rfull[s], 1); mbar_init(&rempty[s], CONVW); }
@@ -293,6 +301,7 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
     int rstage = 0, astage = 0;
     uint32_t rph = 0, aph = 0;
     for (int it = 0; it < nitems; ++it) {
+      if (ares && !gstart(it)) continue;
       float sA = 1.f;
       if constexpr (F16) sA = f16_scale(__ldg(p.amax_in + (w0 + it) / per_z));
       for (int c = 0; c < nchunk; ++c, ++j) {
@@ -487,24 +496,28 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
   } else if (warp == TG_MMA_WARP) {
     // ---------------- MMA issuer ----------------
     const uint32_t idesc = F16 ? f16_idesc(2 * NT) : tf32_idesc(2 * NT);
-    int bi = 0;
+    // ring positions kept as counters (no div/mod on the issue path: at F16
+    // rates the issuer's own instruction latency is what starves the pipe)
+    int bs = 0, stage = 0, acc = 0, stage0 = 0;
+    uint32_t bph = 0, aph = 0, tph = 0, aph0 = 0;
+    const uint64_t dB = umma_desc(smem_u32(bring), 128, SBO_B);   // + (byte offset >> 4) per block
+    const uint32_t bstage16 = (6 * bbytes) >> 4, bblk16 = bbytes >> 4;
     for (int it = 0; it < nitems; ++it) {
-      const int acc = it % TS;
-      mbar_wait_spin(&tempty[acc], ((it / TS) & 1) ^ 1);
+      mbar_wait_spin(&tempty[acc], tph ^ 1);
       tc_fence_after();
       const uint32_t dre = tmem + (uint32_t)(acc * 2 * NT);
-      for (int c = 0; c < nchunk; ++c, ++bi) {
-        const int stage = bi % AS;
-        const int bs = bi % BS;
+      const bool gs = !ares || gstart(it), ge = !ares || gend(it);
+      if (gs) { stage0 = stage; aph0 = aph; }
+      else { stage = stage0; aph = aph0; }         // ares: the group's stages again, same phase
+      for (int c = 0; c < nchunk; ++c) {
         if (!(p.dbg & 1)) {
-          mbar_wait_spin(&afull[stage], (bi / AS) & 1);
-          mbar_wait_spin(&bfull[bs], (bi / BS) & 1);
+          if (gs) mbar_wait_spin(&afull[stage], aph);
+          mbar_wait_spin(&bfull[bs], bph);
         }
         tc_fence_after();
         if (lane == 0) {
-          const uint32_t b0 = smem_u32(bring + (size_t)bs * 6 * bbytes);
-          const uint64_t b2h = umma_desc(b0, 128, SBO_B), b1h = umma_desc(b0 + bbytes, 128, SBO_B);
-          const uint64_t b2l = umma_desc(b0 + 3 * bbytes, 128, SBO_B), b1l = umma_desc(b0 + 4 * bbytes, 128, SBO_B);
+          const uint64_t bb = dB + (uint64_t)(bs * bstage16);
+          const uint64_t b2h = bb, b1h = bb + bblk16, b2l = bb + 3 * bblk16, b1l = bb + 4 * bblk16;
           if constexpr (F16) {
             const uint32_t arh = tmem + A0 + (uint32_t)stage * ACOLS;
             const uint32_t aih = arh + 8, arl = arh + 16, ail = arh + 24;
@@ -530,41 +543,47 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
             mma_tf32_ts(dre, arh, b1h + st, idesc, 1u);
             mma_tf32_ts(dre, aih, b2h + st, idesc, 1u);
           }
-          umma_commit(&aempty[stage]);
+          if (ge) umma_commit(&aempty[stage]);
           umma_commit(&bempty[bs]);
           if (c == nchunk - 1) umma_commit(&tfull[acc]);
         }
         __syncwarp();
+        if (++bs == BS) { bs = 0; bph ^= 1; }
+        if (++stage == AS) { stage = 0; aph ^= 1; }
       }
+      if (++acc == TS) { acc = 0; tph ^= 1; }
     }
   } else if (warp == TG_APROD_WARP && lane == 0 && !(p.dbg & 1)) {
     // ---------------- A producer: TMA tiles into the group's raw slice ----------------
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
-    int j = 0;
+    int j = 0, rs = 0;
+    uint32_t rph = 0;
     for (int it = 0; it < nitems; ++it) {
+      if (ares && !gstart(it)) continue;
       const int64_t w = w0 + it;
       const int64_t z = w / per_z;
       const int64_t mt = (w - z * per_z) / p.tiles_n;
       for (int c = 0; c < nchunk; ++c, ++j) {
-        const int rs = j % RS;
-        mbar_wait_spin(&rempty[rs], ((j / RS) & 1) ^ 1);
+        mbar_wait_spin(&rempty[rs], rph ^ 1);
         mbar_expect_tx(&rfull[rs], RAW_BYTES);
         tma_load_3d(araw + (size_t)rs * RAW_BYTES, &tmA, c * 2 * KC, (int)(mt * 128), (int)z, &rfull[rs]);
+        if (++rs == RS) { rs = 0; rph ^= 1; }
       }
     }
   } else if (warp == TG_BPROD_WARP && lane == 0 && !(p.dbg & 1)) {
     // ---------------- B producer: Br/Bi hi/lo chunks ----------------
-    int bi = 0;
+    int bi = 0, bs = 0;
+    uint32_t bph = 0;
     for (int it = 0; it < nitems; ++it) {
       const int64_t w = w0 + it;
       const int64_t z = w / per_z;
       const int64_t nt = (w - z * per_z) % p.tiles_n;
       const unsigned char* src = p.bp + gemm_combo(p, z) * p.bp_combo_stride + (int64_t)nt * nchunk * 6 * bbytes;
       for (int c = 0; c < nchunk; ++c, ++bi) {
-        const int bs = bi % BS;
-        mbar_wait_spin(&bempty[bs], ((bi / BS) & 1) ^ 1);
+        mbar_wait_spin(&bempty[bs], bph ^ 1);
         mbar_expect_tx(&bfull[bs], 6 * bbytes);
         bulk_g2s(bring + (size_t)bs * 6 * bbytes, src + (int64_t)c * 6 * bbytes, 6 * bbytes, &bfull[bs]);
+        if (++bs == BS) { bs = 0; bph ^= 1; }
       }
     }
   }
@@ -656,9 +675,16 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
     const int f16 = (d.amax_in != nullptr && KC == 16 && tc16_enabled()) ? 1 : 0;
     p.f16 = f16;
     p.amax_in = f16 ? d.amax_in : nullptr;
+    // F16, N >= 128: 128-wide column tiles (N = 256 MMAs: the issuer's
+    // per-chunk overhead stays below the MMA time), one accumulator stage; for
+    // K <= 128 the converted A tile stays resident across column tiles
+    if (f16 && d.N >= 128) {
+      p.NT = 128;
+      p.tiles_n = (int)((d.N + p.NT - 1) / p.NT);
+    }
     if (const char* e = getenv("TNC_TG_NT")) {
       const int nt = atoi(e);
-      if (nt >= 16 && nt % 16 == 0 && nt <= (f16 ? 96 : 64)) {
+      if (nt >= 16 && nt % 16 == 0 && nt <= (f16 ? 128 : 64) && d.N >= nt) {
         p.NT = nt;
         p.tiles_n = (int)((d.N + p.NT - 1) / p.NT);
       }
