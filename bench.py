@@ -238,7 +238,8 @@ def run_sweep(args, rank, world, dev):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": (roof_t / t_kern), "traffic": None,
                      "peak_source": f"{peak_src} hbm_gbs / bf16_tflops (MEASURED_PEAKS.json)",
-                     "kernel": "tnc::k_pair_tiled_* (fused permute+contract)",
+                     "kernel": "all contraction launches of the sweep: tnc::k_tc_c64 (tcgen05 3xTF32, K*N >= 256) "
+                               "and tnc::k_pair_pipe* (TMA-fed fused permute+contract SIMT); projections excluded",
                      "algorithmic": "per case (acc + out + 2*projected site) * 8 B; flops 8*B*2^r*4^k*4^n",
                      "kernel_share_of_step": t_kern / t_case, "tflops_achieved": flops_tot / t_kern / 1e12},
         "config": {"workload": "configs[1] pairwise-contraction sweep", "dtype": "complex64",
@@ -378,8 +379,9 @@ def run_syc53(args, rank, world, dev):
         "gpu_launches": launches * args.steps,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
                      "frac": achieved / bf16, "traffic": None,
-                     "peak_source": f"{peak_src} bf16_tflops (MEASURED_PEAKS.json); the kernel runs 3xTF32",
-                     "kernel": "tnc::k_tc_gemm (tcgen05 3xTF32 complex GEMM steps)",
+                     "peak_source": f"{peak_src} bf16_tflops (MEASURED_PEAKS.json); the kernel issues fp16 MMAs "
+                                    "(3 split products per real product, so 3x the algorithmic flops on the pipe)",
+                     "kernel": "tnc::k_tc_gemm<16,F16> (tcgen05 kind::f16 fp16-split complex GEMM steps)",
                      "algorithmic": "8*M*K*N flops per step per bitstring",
                      "kernel_share_of_step": gemm_t / tot_t if tot_t else None,
                      "path_roofline_frac": tot_roof / tot_t if tot_t else None,
@@ -589,6 +591,8 @@ def main():
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu", dest="cpu", action="store_false")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--no-syc", dest="syc", action="store_false",
+                    help="sweep workload: skip the nested 53-qubit amplitude measurement")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -640,6 +644,20 @@ def main():
     runner = {"sweep": run_sweep, "cfg0": run_cfg0, "syc53": run_syc53}[args.workload]
     res = runner(args, rank, world, dev)
     plan_steps = res.pop("_plan_steps", None)
+    syc = None
+    if args.workload == "sweep" and args.syc:
+        # the headline circuit family, measured beside the sweep: amplitudes/s of
+        # the 53-qubit Sycamore network at the deepest depth one GPU holds
+        sargs = argparse.Namespace(**vars(args))
+        sargs.steps, sargs.warmup = max(3, min(args.steps, 5)), max(3, args.warmup)
+        syc = run_syc53(sargs, rank, world, dev)
+        syc_steps = syc.pop("_plan_steps", None)
+        if rank == 0 and args.cpu and world == 1 and syc_steps:
+            cv, spent = cpu_syc_rate(syc_steps, min(args.cpu_budget, 10.0))
+            syc["cpu_baseline"] = {"value": cv, "unit": "amplitudes/s", "cores": _cpu_threads(), "kind": "port",
+                                   "sample": f"numpy tensordot on 2^14-row samples of every distinct step shape, "
+                                             f"{spent:.1f}s; scaled by rows (permutation cost not included)"}
+        syc["steps"], syc["warmup"] = sargs.steps, sargs.warmup
     if rank == 0:
         if args.cpu and world == 1:
             if args.workload == "sweep":
@@ -656,6 +674,8 @@ def main():
                                                  "scaled by rows (permutation cost not included: favours the CPU)"}
         detail = res.pop("detail", None)
         line = dict(base, **res)
+        if syc is not None:
+            line["amplitudes_53q"] = syc
         print(json.dumps(line))
         if detail is not None:
             (ROOT / "gpurun_out").mkdir(exist_ok=True)

@@ -329,7 +329,7 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
       if ((warp & 3) == 0) TC_TRACE(0, t);
       if (RS > 0) {
         const int rs = t % RS;
-        mbar_wait(&rfull[rs], (uint32_t)((t / RS) & 1));
+        mbar_wait_spin(&rfull[rs], (uint32_t)((t / RS) & 1));
         if ((warp & 3) == 0) TC_TRACE(1, t);
         raw = reinterpret_cast<const float2*>(rawring + (size_t)rs * tc_raw_bytes(p.K)) + looff_s[r];
       }
@@ -347,7 +347,7 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
 #pragma unroll
           for (int q = 0; q < KC; ++q) v[q] = (p.dbg & 2) ? make_float2(1.f, 0.f) : __ldg(Ar + ko[q]);
         }
-        mbar_wait(&empty[stage], ph ^ 1);
+        mbar_wait_spin(&empty[stage], ph ^ 1);
         tc_fence_after();
         const uint32_t col = A0 + (uint32_t)stage * ACOLS;
 #pragma unroll
@@ -390,7 +390,7 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
       const int acc = t % TS;
       const uint32_t ph = (t / TS) & 1;
       if (q == 0) TC_TRACE(3, t);
-      mbar_wait(&tfull[acc], ph);
+      mbar_wait_spin(&tfull[acc], ph);
       if (q == 0) TC_TRACE(4, t);
       tc_fence_after();
       const int64_t gt = g0 + t;
@@ -449,8 +449,17 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
     int it = 0;
     int64_t cur_z = z0;
     uint32_t bdone_phase = 0;
+    // ring positions as counters (no div/mod on the issue path)
+    const int NGm = (AS >= 4 && (RS == 0 || RS % 2 == 0)) ? 2 : 1;
+    const int ASg = AS / NGm;
+    int gpos[2] = {0, 0};
+    uint32_t gph[2] = {0, 0};
+    int acc = 0;
+    uint32_t aph = 0;
+    int64_t zt = z0, zleft = p.tiles_per_z - (g0 - z0 * p.tiles_per_z);
     for (int t = 0; t < ntiles; ++t) {
-      const int64_t zt = (g0 + t) / p.tiles_per_z;
+      if (zleft == 0) { ++zt; zleft = p.tiles_per_z; }
+      --zleft;
       if (zt != cur_z) {
         if (lane == 0) umma_commit(bdone);
         __syncwarp();
@@ -463,21 +472,17 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
         tc_fence_before();
         cur_z = zt;
       }
-      const int acc = t % TS;
-      const uint32_t aph = (t / TS) & 1;
       TC_TRACE(6, t);
-      mbar_wait(&tempty[acc], aph ^ 1);
+      mbar_wait_spin(&tempty[acc], aph ^ 1);
       TC_TRACE(7, t);
       tc_fence_after();
       const uint32_t d = tmem + (uint32_t)(acc * Nr);
+      const int g = NGm == 2 ? (t & 1) : 0;
       for (int c = 0; c < nchunk; ++c, ++it) {
-        const int NGm = (AS >= 4 && (RS == 0 || RS % 2 == 0)) ? 2 : 1;
-        const int ASg = AS / NGm;
-        const int g = t % NGm;
-        const int jj = (t / NGm) * nchunk + c;
-        const int stage = g * ASg + jj % ASg;
-        const uint32_t ph = (jj / ASg) & 1;
-        mbar_wait(&full[stage], ph);
+        const int stage = g * ASg + gpos[g];
+        const uint32_t ph = gph[g];
+        if (++gpos[g] == ASg) { gpos[g] = 0; gph[g] ^= 1; }
+        mbar_wait_spin(&full[stage], ph);
         TC_TRACE(8, it);
         tc_fence_after();
         if (lane == 0) {
@@ -502,14 +507,18 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
         __syncwarp();
         TC_TRACE(9, it);
       }
+      if (++acc == TS) { acc = 0; aph ^= 1; }
     }
   } else if (warp == TC_PROD_WARP && RS > 0 && lane == 0) {
     // ---------------- raw-ring producer: cp.async.bulk of each tile's segments ----------------
     const uint32_t seg_bytes = (uint32_t)(p.Lseg * 8);
+    int rs = -1;
+    uint32_t rph = 1;
     for (int t = 0; t < ntiles; ++t) {
-      const int rs = t % RS;
+      if (++rs == RS) rs = 0;
+      if (rs == 0) rph ^= 1;
       TC_TRACE(12, t);
-      mbar_wait(&rempty[rs], (uint32_t)(((t / RS) & 1) ^ 1));
+      mbar_wait_spin(&rempty[rs], rph ^ 1);
       TC_TRACE(13, t);
       unsigned char* dst = rawring + (size_t)rs * tc_raw_bytes(p.K);
       const float2* src = p.a + tbase[t];
