@@ -77,11 +77,43 @@ void skinny_row(const tnc_step_desc& d, cudaStream_t s) {
   tnc::k_step_skinny_row<R, KMAX><<<(unsigned)((rows + 127) / 128), 128, 0, s>>>(d);
 }
 
+template <int L>
+void warp_step(const tnc_step_desc& d, cudaStream_t s) {
+  // grid: x over row groups of one z, y over z; about 16 warps-worth per SM in total
+  const int64_t zb = std::min<int64_t>(d.Z, 65535);
+  const int64_t warps_needed = (d.M + (32 / L) * 4 - 1) / ((32 / L) * 4);
+  const int64_t bx = std::max<int64_t>(1, std::min<int64_t>((warps_needed + 7) / 8, (148 * 16 + zb - 1) / zb));
+  const dim3 grid((unsigned)bx, (unsigned)zb);
+  if (d.N <= 1) tnc::k_step_warp<L, 1><<<grid, 256, 0, s>>>(d);
+  else if (d.N <= 2) tnc::k_step_warp<L, 2><<<grid, 256, 0, s>>>(d);
+  else if (d.N <= 4) tnc::k_step_warp<L, 4><<<grid, 256, 0, s>>>(d);
+  else if (d.N <= 8) tnc::k_step_warp<L, 8><<<grid, 256, 0, s>>>(d);
+  else tnc::k_step_warp<L, 16><<<grid, 256, 0, s>>>(d);
+}
+
 template <typename R>
 bool try_skinny(const tnc_step_desc& d, cudaStream_t s) {
   if (!d.a_rows_contig || !d.b_dense || d.conj_b) return false;
   if (d.Z * d.M > (int64_t)0x7fffffff * 128) return false;
   const int64_t N = d.N, K = d.K;
+  // few rows (path ends: tiny M, large K or N): one thread per result element
+  if (d.Z * d.M < 4096) {
+    tnc::k_step_cols<R><<<grid_for(d.Z * d.M * N, 256), 256, 0, s>>>(d);
+    return true;
+  }
+  // complex64, K = 2..64 (power of two), N <= 16: warp-cooperative coalesced rows
+  if (sizeof(R) == 4 && N <= 16 && K * N < 256 && K >= 2 && K <= 64 && (K & (K - 1)) == 0 &&
+      ((uintptr_t)d.acc % 16) == 0 && (d.acc_zstride % 2) == 0 && d.M < 0x7fffffffLL &&
+      d.out_zstride < 0x7fffffffLL) {
+    switch (K) {
+      case 2: warp_step<1>(d, s); return true;
+      case 4: warp_step<2>(d, s); return true;
+      case 8: warp_step<4>(d, s); return true;
+      case 16: warp_step<8>(d, s); return true;
+      case 32: warp_step<16>(d, s); return true;
+      default: warp_step<32>(d, s); return true;
+    }
+  }
   if (N <= 32) {
     if (N <= 1) skinny_acc<R, 1>(d, s);
     else if (N <= 2) skinny_acc<R, 2>(d, s);

@@ -251,6 +251,156 @@ k_slice_sum(const __grid_constant__ tnc_slice_sum_desc d) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Few-row steps (Z*M small, e.g. the first and last steps of a path, where M
+// is tiny and N or K large): one thread per result element, so the launch
+// still spans the GPU.  The row of acc is a warp-wide broadcast, the site
+// column is read coalesced across consecutive n.
+// ---------------------------------------------------------------------------
+template <typename R>
+__global__ void __launch_bounds__(256)
+k_step_cols(const __grid_constant__ tnc_step_desc d) {
+  using C = typename cplx<R>::T;
+  const int64_t total = d.Z * d.M * d.N;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t zf = g / d.N, n = g - zf * d.N;
+    const int64_t z = zf / d.M, f = zf - z * d.M;
+    const C* a = reinterpret_cast<const C*>(d.acc) + z * d.acc_zstride + f * d.K;
+    const C* S = reinterpret_cast<const C*>(d.site.ptr) + site_offset(d.site, z, d.slices_per_b, d.s0) + n;
+    C acc = czero<R>();
+    for (int64_t k = 0; k < d.K; ++k) {
+      C b = __ldg(S + k * d.N);
+      if (d.conj_b) b = cconj(b);
+      cfma(acc, __ldg(a + k), b);
+    }
+    C* o = reinterpret_cast<C*>(d.out) + z * d.out_zstride;
+    if (d.c_rows_contig) {
+      o[f * d.N + n] = acc;
+    } else {
+      int64_t oa, oc;
+      row_offsets(d, f, oa, oc);
+      o[oc + d.c_noff[n]] = acc;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Warp-cooperative skinny step (complex64, K = 2L in {2..64}, N <= NN <= 4):
+// L lanes share one acc row, each loading 16 contiguous bytes (two complex),
+// so every warp load is a coalesced 512-byte stream of 32/L whole rows; the
+// N partial sums are reduced across the L lanes with xor shuffles.  UNR row
+// groups per iteration keep several loads in flight per warp.
+// ---------------------------------------------------------------------------
+// 32-bit mixed-radix row decomposition (all extents and offsets < 2^31)
+__device__ __forceinline__ uint32_t row_cout32(const tnc_step_desc& d, uint32_t f) {
+  uint32_t oc = 0;
+  for (int j = d.nf - 1; j >= 0; --j) {
+    const uint32_t dm = (uint32_t)d.f_dim[j];
+    const uint32_t q = f / dm;
+    oc += (f - q * dm) * (uint32_t)d.f_cstride[j];
+    f = q;
+  }
+  return oc;
+}
+
+template <int L, int NN>
+__global__ void __launch_bounds__(256)
+k_step_warp(const __grid_constant__ tnc_step_desc d) {
+  constexpr int RP = 32 / L;                 // rows per warp pass
+  constexpr int UNR = NN >= 8 ? 2 : 4;       // passes in flight per warp
+  constexpr int OWN = NN >= L ? NN / L : 1;  // results owned by a lane after the reduction
+  const int lane = threadIdx.x & 31;
+  const int j = lane % L;                    // complex pair index within the row
+  const int rg = lane / L;                   // row within the pass
+  const int N = (int)d.N;
+  const uint32_t M = (uint32_t)d.M;
+  const uint32_t wpb = blockDim.x >> 5;
+  const uint32_t wstride = gridDim.x * wpb * RP * UNR;
+  const uint32_t wbase = (blockIdx.x * wpb + (threadIdx.x >> 5)) * RP * UNR;
+  // results n0 .. n0 + OWN - 1 of each row end up in this lane
+  const int n0 = NN >= L ? j * OWN : j;
+  for (int64_t z = blockIdx.y; z < d.Z; z += gridDim.y) {
+    const float4* Az = reinterpret_cast<const float4*>(reinterpret_cast<const float2*>(d.acc) + z * d.acc_zstride);
+    float2* Oz = reinterpret_cast<float2*>(d.out) + z * d.out_zstride;
+    const float2* S = reinterpret_cast<const float2*>(d.site.ptr) + site_offset(d.site, z, d.slices_per_b, d.s0) +
+                      (int64_t)(2 * j) * N;
+    float2 s0[NN], s1[NN];                   // this lane's two site rows, for the whole z
+#pragma unroll
+    for (int n = 0; n < NN; ++n) {
+      s0[n] = n < N ? __ldg(S + n) : make_float2(0.f, 0.f);
+      s1[n] = n < N ? __ldg(S + N + n) : make_float2(0.f, 0.f);
+    }
+    for (uint32_t base = wbase; base < M; base += wstride) {
+      float4 av[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const uint32_t f = base + u * RP + rg;
+        av[u] = f < M ? __ldg(Az + (size_t)f * L + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        float2 v[NN];
+#pragma unroll
+        for (int n = 0; n < NN; ++n) {
+          v[n] = make_float2(0.f, 0.f);
+          cfma(v[n], make_float2(av[u].x, av[u].y), s0[n]);
+          cfma(v[n], make_float2(av[u].z, av[u].w), s1[n]);
+        }
+        if constexpr (NN >= L) {
+          // reduce-scatter: each halving step keeps the half selected by one
+          // bit of j (most significant first), so lane j ends with n in
+          // [j*OWN, (j+1)*OWN)
+          int cnt = NN;
+#pragma unroll
+          for (int off = L / 2; off > 0; off >>= 1) {
+            const bool up = (j & off) != 0;
+            cnt >>= 1;
+#pragma unroll
+            for (int i = 0; i < NN / 2; ++i) {
+              if (i < cnt) {
+                const float2 lo = v[i], hi = v[i + cnt];
+                const float2 send = up ? lo : hi;
+                float2 recv;
+                recv.x = __shfl_xor_sync(0xffffffffu, send.x, off);
+                recv.y = __shfl_xor_sync(0xffffffffu, send.y, off);
+                const float2 keep = up ? hi : lo;
+                v[i] = make_float2(keep.x + recv.x, keep.y + recv.y);
+              }
+            }
+          }
+        } else {
+#pragma unroll
+          for (int off = L / 2; off > 0; off >>= 1) {
+#pragma unroll
+            for (int n = 0; n < NN; ++n) {
+              v[n].x += __shfl_xor_sync(0xffffffffu, v[n].x, off);
+              v[n].y += __shfl_xor_sync(0xffffffffu, v[n].y, off);
+            }
+          }
+          // lane j keeps result j
+#pragma unroll
+          for (int n = 1; n < NN; ++n)
+            if (j == n) v[0] = v[n];
+        }
+        const uint32_t f = base + u * RP + rg;
+        if (f < M && n0 < N) {
+          if (d.c_rows_contig) {
+            float2* o = Oz + (size_t)f * N + n0;
+#pragma unroll
+            for (int i = 0; i < OWN; ++i)
+              if (n0 + i < N) o[i] = v[i];
+          } else {
+            const uint32_t oc = row_cout32(d, f);
+#pragma unroll
+            for (int i = 0; i < OWN; ++i)
+              if (n0 + i < N) Oz[oc + (uint32_t)d.c_noff[n0 + i]] = v[i];
+          }
+        }
+      }
+    }
+  }
+}
+
 // amax[z] = max |re|, |im| over x[z * zstride + i], i < count (atomicMax on
 // the float bits: non-negative floats order like their bit patterns)
 __global__ void k_amax(const float2* __restrict__ x, int64_t Z, int64_t zstride, int64_t count, float* amax) {

@@ -109,7 +109,8 @@ __device__ __forceinline__ void split_f16x2(float y0, float y1, uint32_t& h, uin
   asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(l) : "f"(l1), "f"(l0));
 }
 
-// per combo: max |re|, |im| over the site block (F16 scale of B')
+// per combo (blockIdx.x): max |re|, |im| over the site block (F16 scale of
+// B'); blockIdx.y strides over K rows, atomicMax into the zeroed bscale
 __global__ void k_bscale(const __grid_constant__ GemmDesc p, float* bscale) {
   const int64_t combo = blockIdx.x;
   int64_t off = 0, cc = combo;
@@ -120,19 +121,15 @@ __global__ void k_bscale(const __grid_constant__ GemmDesc p, float* bscale) {
   off += cc * p.site.vstride;
   const float2* S = reinterpret_cast<const float2*>(p.site.ptr) + off;
   float m = 0.f;
-  for (int64_t e = threadIdx.x; e < p.K * p.N; e += blockDim.x) {
-    const int64_t k = e / p.N, n = e - k * p.N;
-    const float2 v = S[p.b_koff[k] + p.b_noff[n]];
-    m = fmaxf(m, fmaxf(fabsf(v.x), fabsf(v.y)));
+  for (int64_t k = blockIdx.y; k < p.K; k += gridDim.y) {
+    const float2* Sk = S + p.b_koff[k];
+    for (int64_t n = threadIdx.x; n < p.N; n += blockDim.x) {
+      const float2 v = Sk[p.b_noff[n]];
+      m = fmaxf(m, fmaxf(fabsf(v.x), fabsf(v.y)));
+    }
   }
   for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  __shared__ float red[32];
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, red[w]);
-    bscale[combo] = m;
-  }
+  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(reinterpret_cast<unsigned int*>(bscale) + combo, __float_as_uint(m));
 }
 
 // Site operand for every (combo, N tile, K chunk): hi then lo, each three
@@ -738,7 +735,9 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
       int blocks = (int)std::min<int64_t>((work + 255) / 256, 148 * 16);
       if (f16) {
         float* bsc = reinterpret_cast<float*>(bp + bp_bytes);
-        k_bscale<<<(unsigned)combos, 256, 0, s>>>(p, bsc);
+        if (cudaMemsetAsync(bsc, 0, combos * 4, s) != cudaSuccess) return -1;
+        const unsigned ky = (unsigned)std::min<int64_t>(d.K, std::max<int64_t>(1, 296 / combos));
+        k_bscale<<<dim3((unsigned)combos, ky), d.N >= 256 ? 256 : 128, 0, s>>>(p, bsc);
         p.bscale = bsc;
         k_bprime<true><<<blocks < 1 ? 1 : blocks, 256, 0, s>>>(p, combos);
       } else {

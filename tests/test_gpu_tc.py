@@ -191,3 +191,45 @@ def test_tc_gemm_f16_split_step(M, K, N, scale):
     assert err <= 2e-6, err
     want = torch.view_as_real(out.reshape(Z, -1)).abs().reshape(Z, -1).amax(dim=1)
     assert torch.equal(amax_out, want), (amax_out, want)
+
+
+@pytest.mark.parametrize("dtype", ["complex64", "complex128"])
+@pytest.mark.parametrize("M,K,N", [(65536, 16, 1), (65536, 8, 4), (65536, 2, 2), (65536, 64, 3), (131072, 32, 2), (65536, 8, 16), (65536, 4, 8), (65536, 2, 16), (65536, 16, 12),
+                                   (4, 16, 2048), (32, 2048, 16), (1, 512, 2)])
+def test_skinny_and_few_row_steps(M, K, N, dtype):
+    """Warp-cooperative skinny kernel (complex64, K <= 64, N <= 4) and the
+    few-row kernel (Z*M < 4096) against the complex128 product of the same
+    operands, through tnc_step with automatic kernel choice."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2011_02621_b200 import _native as NV
+    from paper_2011_02621_b200.engine import ContractionPlan, NetworkSpec, PathExecutor
+
+    edges = {(0, 1): K, (0, 2): M, (1, 2): N}
+    legs = {0: [(0, 2), (0, 1)], 1: [(0, 1), (1, 2)], 2: [(0, 2), (1, 2)]}
+    spec = NetworkSpec([0, 1, 2], edges, legs)
+    tdt = getattr(torch, dtype)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(M * 7 + K * 3 + N)
+    sites = {q: torch.randn((1,) + spec.site_dims(q), dtype=tdt, device="cuda", generator=g) for q in range(3)}
+    plan = ContractionPlan(spec, [0, 1, 2])
+    sp = plan.steps[0]
+    assert (sp.M, sp.K, sp.N) == (M, K, N)
+    ex = PathExecutor(plan, sites, dtype=dtype)
+    d = ex._steps[0]
+    Z = 3
+    acc = torch.randn(Z * M * K, dtype=tdt, device="cuda", generator=g)
+    out = torch.zeros(Z * M * N, dtype=tdt, device="cuda")
+    d.Z, d.slices_per_b, d.s0 = Z, 1, 0
+    d.acc, d.acc_zstride = acc.data_ptr(), M * K
+    d.out, d.out_zstride = out.data_ptr(), M * N
+    d.site.sel = None
+    d.amax_in = d.amax_out = None
+    NV.check(NV.lib().tnc_step(C.byref(d), C.c_void_p(torch.cuda.current_stream().cuda_stream)), "tnc_step")
+    torch.cuda.synchronize()
+    site = ex.step_sites[0][0][0].reshape(K, N).to(torch.complex128)
+    ref = acc.reshape(Z, M, K).to(torch.complex128) @ site
+    err = ((out.reshape(Z, M, N).to(torch.complex128) - ref).norm() / ref.norm()).item()
+    assert err <= (2e-6 if dtype == "complex64" else 1e-13), err
