@@ -297,10 +297,14 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
     int j = 0;
     int rstage = 0, astage = 0;
     uint32_t rph = 0, aph = 0;
+    float sA = 1.f;
+    int64_t sz = -1;                             // z whose scale sA holds (z changes rarely)
     for (int it = 0; it < nitems; ++it) {
       if (ares && !gstart(it)) continue;
-      float sA = 1.f;
-      if constexpr (F16) sA = f16_scale(__ldg(p.amax_in + (w0 + it) / per_z));
+      if constexpr (F16) {
+        const int64_t zz = (w0 + it) / per_z;
+        if (zz != sz) { sz = zz; sA = f16_scale(__ldg(p.amax_in + zz)); }
+      }
       for (int c = 0; c < nchunk; ++c, ++j) {
         mbar_wait_spin(&rfull[rstage], rph);
         const uint32_t src = smem_u32(araw + (size_t)rstage * RAW_BYTES);
@@ -379,13 +383,25 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
     // innermost result leg is a free leg: consecutive rows are contiguous)
     const bool staged = p.c_rows_contig || p.n_contig || (p.N > 1 && p.c_noff[1] == p.c_noff[0] + 1);
     const int cfirst = alt ? 0 : eg * 16, cstep = alt ? 16 : 16 * EPIG;
+    float inv = 1.f;
+    int64_t inv_z = -1;
+    const uint32_t stg_s = smem_u32(stg);
     for (int it = alt ? eg : 0; it < nitems; it += alt ? EPIG : 1) {
       const int acc = it % TS;
       const uint32_t ph = (it / TS) & 1;
-      const int64_t w = w0 + it;
-      const int64_t z = w / per_z;
-      const int64_t rem = w - z * per_z;
-      const int64_t mt = rem / p.tiles_n, nt = rem - mt * p.tiles_n;
+      int64_t z, mt, nt;
+      {
+        const int64_t w = w0 + it;
+        if (p.items < 0x7fffffffLL) {
+          const uint32_t w32 = (uint32_t)w, pz = (uint32_t)per_z, tn = (uint32_t)p.tiles_n;
+          const uint32_t z32 = w32 / pz, rem = w32 - z32 * pz, m32 = rem / tn;
+          z = z32; mt = m32; nt = rem - m32 * tn;
+        } else {
+          z = w / per_z;
+          const int64_t rem = w - z * per_z;
+          mt = rem / p.tiles_n; nt = rem - mt * p.tiles_n;
+        }
+      }
       const int64_t row = mt * 128 + r;
       int64_t oc = row * p.N;
       if (!p.c_rows_contig && row < p.M) {
@@ -399,8 +415,13 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
       }
       float2* O = p.out + z * p.out_zstride;
       const int64_t n0 = nt * NT;
-      float inv = 1.f, vmax = 0.f;
-      if constexpr (F16) inv = 1.f / (f16_scale(__ldg(p.amax_in + z)) * f16_scale(__ldg(p.bscale + gemm_combo(p, z))));
+      float vmax = 0.f;
+      if constexpr (F16) {
+        if (z != inv_z) {                        // the per-z scales change rarely: reload only then
+          inv_z = z;
+          inv = 1.f / (f16_scale(__ldg(p.amax_in + z)) * f16_scale(__ldg(p.bscale + gemm_combo(p, z))));
+        }
+      }
       mbar_wait(&tfull[acc], ph);
       tc_fence_after();
       const uint32_t tre = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 2 * NT);
@@ -436,7 +457,8 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
           for (int jj = 0; jj < 16; jj += 2) {
             const float4 v = make_float4(__uint_as_float(vr[jj]), __uint_as_float(vi[jj]),
                                          __uint_as_float(vr[jj + 1]), __uint_as_float(vi[jj + 1]));
-            *reinterpret_cast<float4*>(stg + lane * TG_EPI_PITCH + jj * 8) = v;
+            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(stg_s + lane * TG_EPI_PITCH + jj * 8),
+                         "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
           }
           __syncwarp();
           const int sub = lane & 7;                // 16-byte piece (2 complex) of a row
@@ -450,7 +472,9 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
             const int64_t grow = mt * 128 + q * 32 + lr;
             const int64_t ocr = __shfl_sync(0xffffffffu, oc, lr);
             if (grow < p.M && 2 * sub < ncols) {
-              const float4 v = *reinterpret_cast<const float4*>(stg + lr * TG_EPI_PITCH + sub * 16);
+              float4 v;
+              asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                           : "r"(stg_s + lr * TG_EPI_PITCH + sub * 16) : "memory");
               float2* dst = O + ocr + a0;
               if (2 * sub + 1 < ncols && a1 == a0 + 1 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
                 *reinterpret_cast<float4*>(dst) = v;
