@@ -109,6 +109,13 @@ typedef struct {
    * fp16 hi/lo pairs (two-fold MMA rate, same ~2^-22 product accuracy). */
   float*       amax_out;
   const float* amax_in;
+  /* Optional structure of the new legs (nn = 0: unknown): n in [0, N) is
+   * mixed-radix over n_dim (outermost first) and c_noff[n] = n_cstride.n.
+   * Lets the tensor-core epilogue store result tiles with TMA. */
+  int32_t  nn;
+  int32_t  _pad2;
+  int64_t  n_dim[TNC_MAX_LEGS];
+  int64_t  n_cstride[TNC_MAX_LEGS];
 } tnc_step_desc;
 
 /* Gather: out[z][i] = site(z)[ sum_j digit_j(i) * src_stride[j] ], i mixed-radix

@@ -52,6 +52,8 @@ class StepDesc(C.Structure):
         ("a_koff", C.c_void_p), ("b_koff", C.c_void_p), ("b_noff", C.c_void_p), ("c_noff", C.c_void_p),
         ("a_rows_contig", C.c_int32), ("c_rows_contig", C.c_int32), ("b_dense", C.c_int32),
         ("conj_b", C.c_int32), ("amax_out", C.c_void_p), ("amax_in", C.c_void_p),
+        ("nn", C.c_int32), ("_pad2", C.c_int32),
+        ("n_dim", C.c_int64 * MAX_LEGS), ("n_cstride", C.c_int64 * MAX_LEGS),
     ]
 
 

@@ -64,6 +64,17 @@ struct GemmDesc {
   int32_t nf, c_rows_contig;
   int64_t f_dim[TNC_MAX_LEGS], f_cstride[TNC_MAX_LEGS];
   const int64_t* c_noff;         // [N]
+  // TMA-store epilogue (tma_out): each warp's 32 rows x 16 columns block is
+  // staged in smem in the box order of tensor map tmO and stored by one
+  // cp.async.bulk.tensor; o_roff / o_coff give the staging element offset of
+  // row r / column c, *_tdim / *_tmul map every leg digit to a map coordinate
+  int32_t tma_out, o_swz;
+  int32_t o_rank, nn;
+  int16_t o_roff[32], o_coff[16];
+  int8_t f_tdim[TNC_MAX_LEGS], n_tdim[TNC_MAX_LEGS];
+  int32_t f_tmul[TNC_MAX_LEGS], n_tmul[TNC_MAX_LEGS];
+  int64_t n_dim[TNC_MAX_LEGS];
+  int32_t z_tdim, z_tmul;
 };
 
 constexpr int TG_THREADS = 15 * 32;
@@ -194,6 +205,33 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
 }
 
 
+// TMA tensor store of one staged box (rank 1..5), committed as its own bulk group
+__device__ __forceinline__ void tma_store(const CUtensorMap* m, int rank, const int32_t (&c)[5], uint32_t src) {
+  const uint64_t mp = reinterpret_cast<uint64_t>(m);
+  switch (rank) {
+    case 1:
+      asm volatile("cp.async.bulk.tensor.1d.global.shared::cta.tile.bulk_group [%0, {%1}], [%2];"
+                   ::"l"(mp), "r"(c[0]), "r"(src) : "memory");
+      break;
+    case 2:
+      asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];"
+                   ::"l"(mp), "r"(c[0]), "r"(c[1]), "r"(src) : "memory");
+      break;
+    case 3:
+      asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];"
+                   ::"l"(mp), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(src) : "memory");
+      break;
+    case 4:
+      asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4}], [%5];"
+                   ::"l"(mp), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(src) : "memory");
+      break;
+    default:
+      asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];"
+                   ::"l"(mp), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(src) : "memory");
+  }
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
 __device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
                                            uint32_t accumulate) {
   asm volatile(
@@ -209,7 +247,8 @@ __device__ __forceinline__ uint32_t f16_idesc(int n_real) {
 
 template <int KC, bool F16>
 __global__ void __launch_bounds__(TG_THREADS, 1)
-k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMap tmA) {
+k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMap tmA,
+          const __grid_constant__ CUtensorMap tmO) {
   static_assert(!F16 || KC == 16, "F16 mode needs 16-complex chunks (K = 16 per MMA)");
   extern __shared__ __align__(128) unsigned char smem_dyn[];
   constexpr int RB = KC * 8;                       // raw row bytes (KC complex)
@@ -245,8 +284,8 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
   // smem: raw A ring (1024-aligned stages: swizzle atoms), B ring, epilogue staging, barriers
   unsigned char* araw = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
   unsigned char* bring = araw + (size_t)RS * RAW_BYTES;
-  unsigned char* estage = bring + (size_t)BS * 6 * bbytes;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(estage + EPIW * 32 * TG_EPI_PITCH);
+  unsigned char* estage = bring + (size_t)BS * 6 * bbytes;   // 1024-aligned (stage sizes are KB multiples)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(estage + (p.tma_out ? EPIW * 8192 : EPIW * 32 * TG_EPI_PITCH));
   uint64_t* rfull = bar;                           // [RS] TMA -> converters
   uint64_t* rempty = rfull + TG_MAX_RS;            // [RS] converters -> TMA
   uint64_t* afull = rempty + TG_MAX_RS;            // [AS] converters -> MMA
@@ -386,6 +425,8 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
     float inv = 1.f;
     int64_t inv_z = -1;
     const uint32_t stg_s = smem_u32(stg);
+    const uint32_t ostage_s = smem_u32(estage);
+    int oblk = 0;
     for (int it = alt ? eg : 0; it < nitems; it += alt ? EPIG : 1) {
       const int acc = it % TS;
       const uint32_t ph = (it / TS) & 1;
@@ -448,6 +489,51 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
           vi[jj] = __float_as_uint(b);
         }
         if (p.dbg & 4) continue;                 // debug: TMEM loads only
+        if (p.tma_out) {
+          if (n0 + c0 >= p.N) continue;
+          // double-buffered 4 KB staging per warp; the store that last read
+          // this buffer must have finished reading it
+          const uint32_t sb = ostage_s + (uint32_t)(warp - CONVW) * 8192u + (uint32_t)(oblk & 1) * 4096u;
+          ++oblk;
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          __syncwarp();
+          const int ro = p.o_roff[lane];
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) {
+            uint32_t e = (uint32_t)(ro + p.o_coff[jj]);
+            if (p.o_swz) e = (e & ~15u) | ((((e >> 1) & 7u) ^ ((e >> 4) & 7u)) << 1) | (e & 1u);
+            asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(sb + e * 8u), "f"(__uint_as_float(vr[jj])),
+                         "f"(__uint_as_float(vi[jj])) : "memory");
+          }
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0) {
+            int32_t cr[5] = {0, 0, 0, 0, 0};
+            uint32_t f = (uint32_t)(mt * 128 + q * 32);
+            for (int jl = p.nf - 1; jl >= 0; --jl) {
+              const uint32_t dm = (uint32_t)p.f_dim[jl], qq = f / dm;
+              const int32_t add = (int32_t)(f - qq * dm) * p.f_tmul[jl];
+              f = qq;
+              switch (p.f_tdim[jl]) { case 0: cr[0] += add; break; case 1: cr[1] += add; break;
+                                      case 2: cr[2] += add; break; case 3: cr[3] += add; break; default: cr[4] += add; }
+            }
+            uint32_t nn_ = (uint32_t)(n0 + c0);
+            for (int jl = p.nn - 1; jl >= 0; --jl) {
+              const uint32_t dm = (uint32_t)p.n_dim[jl], qq = nn_ / dm;
+              const int32_t add = (int32_t)(nn_ - qq * dm) * p.n_tmul[jl];
+              nn_ = qq;
+              switch (p.n_tdim[jl]) { case 0: cr[0] += add; break; case 1: cr[1] += add; break;
+                                      case 2: cr[2] += add; break; case 3: cr[3] += add; break; default: cr[4] += add; }
+            }
+            {
+              const int32_t add = (int32_t)z * p.z_tmul;
+              switch (p.z_tdim) { case 0: cr[0] += add; break; case 1: cr[1] += add; break;
+                                  case 2: cr[2] += add; break; case 3: cr[3] += add; break; default: cr[4] += add; }
+            }
+            tma_store(&tmO, p.o_rank, cr, sb);
+          }
+          continue;
+        }
         const int64_t nleft = p.N - (n0 + c0);
         const int ncols = nleft < 16 ? (int)nleft : 16;
         if (staged) {
@@ -514,6 +600,7 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
         if (lane == 0 && vmax > 0.f) atomicMax(reinterpret_cast<unsigned int*>(p.amax_out) + z, __float_as_uint(vmax));
       }
     }
+    if (p.tma_out && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   } else if (warp == TG_MMA_WARP) {
     // ---------------- MMA issuer ----------------
     const uint32_t idesc = F16 ? f16_idesc(2 * NT) : tf32_idesc(2 * NT);
@@ -616,8 +703,9 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
   }
 }
 
-__host__ inline size_t tg_smem_bytes(int NT, int KC, int RS, int BS, int f16, int64_t cn = 0) {
-  return 1024 + (size_t)RS * 128 * KC * 8 + (size_t)BS * 6 * tg_block_bytes(NT, KC, f16) + (f16 ? 8 : 4) * 32 * TG_EPI_PITCH +
+__host__ inline size_t tg_smem_bytes(int NT, int KC, int RS, int BS, int f16, int64_t cn = 0, int tma = 0) {
+  return 1024 + (size_t)RS * 128 * KC * 8 + (size_t)BS * 6 * tg_block_bytes(NT, KC, f16) +
+         (size_t)(f16 ? 8 : 4) * (tma ? 8192 : 32 * TG_EPI_PITCH) +
          8 * (2 * TG_MAX_RS + 2 * TC_MAX_STAGES + 2 * TG_MAX_BS + 8) + 16 + 4 * cn;
 }
 
@@ -637,6 +725,121 @@ inline tg_encode_fn tg_encoder() {
       fn = reinterpret_cast<tg_encode_fn>(f);
   }
   return fn;
+}
+
+// Tensor map for the TMA-store epilogue: the result legs (free legs, new legs,
+// batch z) sorted by stride must nest densely; legs are merged into <= 5 map
+// dimensions so that every warp block (32 rows x 16 columns, aligned) is one
+// box.  Fills the tma_out fields of p; false = keep the register/LSU stores.
+inline bool tg_out_map(const tnc_step_desc& d, GemmDesc& p, CUtensorMap& tm, tg_encode_fn enc) {
+  p.tma_out = 0;
+  // opt-in (TNC_TG_TMAOUT=1): measured slower than the LSU stores on the 53q
+  // steps (one in-flight box per warp buffer; strided 256-byte box rows)
+  {
+    const char* e = getenv("TNC_TG_TMAOUT");
+    if (!e || e[0] != '1') return false;
+  }
+  if (d.nn <= 0 || d.nn > TNC_MAX_LEGS || d.nf <= 0) return false;
+  if (d.M % 128 || d.N % 16 || p.NT % 16 || d.out_zstride != d.M * d.N) return false;
+  struct Leg { int64_t dim, stride, box; int kind, idx, tdim; int64_t mult; };
+  std::vector<Leg> legs;
+  auto pow2 = [](int64_t x) { return x > 0 && (x & (x - 1)) == 0; };
+  for (int j = 0; j < d.nf; ++j) {
+    if (!pow2(d.f_dim[j])) return false;
+    legs.push_back({d.f_dim[j], d.f_cstride[j], 1, 0, j, 0, 1});
+  }
+  for (int i = 0; i < d.nn; ++i) {
+    if (!pow2(d.n_dim[i])) return false;
+    legs.push_back({d.n_dim[i], d.n_cstride[i], 1, 1, i, 0, 1});
+  }
+  legs.push_back({d.Z, d.out_zstride, 1, 2, 0, 0, 1});
+  // block extents: 32 rows over the innermost free legs, 16 columns over the innermost new legs
+  {
+    int64_t rem = 32;
+    for (int j = d.nf - 1; j >= 0 && rem > 1; --j) { const int64_t e = std::min(d.f_dim[j], rem); legs[j].box = e; rem /= e; }
+    if (rem > 1) return false;
+    rem = 16;
+    for (int i = d.nn - 1; i >= 0 && rem > 1; --i) { const int64_t e = std::min(d.n_dim[i], rem); legs[d.nf + i].box = e; rem /= e; }
+    if (rem > 1) return false;
+  }
+  std::vector<int> ord;
+  for (int i = 0; i < (int)legs.size(); ++i) if (legs[i].dim > 1 || legs[i].box > 1) ord.push_back(i);
+  std::sort(ord.begin(), ord.end(), [&](int a, int b) { return legs[a].stride < legs[b].stride; });
+  if (ord.empty() || legs[ord[0]].stride != 1) return false;
+  for (size_t k = 1; k < ord.size(); ++k)
+    if (legs[ord[k]].stride != legs[ord[k - 1]].stride * legs[ord[k - 1]].dim) return false;
+  // merge into map dimensions
+  struct Dim { int64_t ext, stride, box; };
+  std::vector<Dim> dims;
+  for (int li : ord) {
+    Leg& L = legs[li];
+    if (!dims.empty()) {
+      Dim& c = dims.back();
+      if ((L.box == 1 || c.box == c.ext) && c.ext * L.dim < (1LL << 31)) {
+        L.tdim = (int)dims.size() - 1;
+        L.mult = c.ext;
+        c.box *= L.box;
+        c.ext *= L.dim;
+        continue;
+      }
+    }
+    L.tdim = (int)dims.size();
+    L.mult = 1;
+    dims.push_back({L.dim, L.stride, L.box});
+  }
+  if (dims.size() > 5) return false;
+  for (auto& dm : dims) if (dm.box > 256 || dm.ext >= (1LL << 31)) return false;
+  if (dims[0].box < 2) return false;
+  // staging offsets (box order, dims[0] innermost)
+  int64_t bstride[5] = {1, 1, 1, 1, 1};
+  for (size_t k = 1; k < dims.size(); ++k) bstride[k] = bstride[k - 1] * dims[k - 1].box;
+  for (int r = 0; r < 32; ++r) {
+    int64_t rr = r, off = 0;
+    for (int j = d.nf - 1; j >= 0; --j) {
+      const Leg& L = legs[j];
+      if (L.box <= 1) continue;
+      off += (rr % L.box) * L.mult * bstride[L.tdim];
+      rr /= L.box;
+    }
+    p.o_roff[r] = (int16_t)off;
+  }
+  for (int c = 0; c < 16; ++c) {
+    int64_t cc = c, off = 0;
+    for (int i = d.nn - 1; i >= 0; --i) {
+      const Leg& L = legs[d.nf + i];
+      if (L.box <= 1) continue;
+      off += (cc % L.box) * L.mult * bstride[L.tdim];
+      cc /= L.box;
+    }
+    p.o_coff[c] = (int16_t)off;
+  }
+  for (int j = 0; j < d.nf; ++j) { p.f_tdim[j] = (int8_t)legs[j].tdim; p.f_tmul[j] = (int32_t)legs[j].mult; }
+  for (int i = 0; i < d.nn; ++i) {
+    p.n_tdim[i] = (int8_t)legs[d.nf + i].tdim; p.n_tmul[i] = (int32_t)legs[d.nf + i].mult; p.n_dim[i] = d.n_dim[i];
+  }
+  p.nn = d.nn;
+  p.z_tdim = legs.back().tdim;
+  p.z_tmul = (int32_t)legs.back().mult;
+  // 128B swizzle when the inner box is one 128-byte run of result columns
+  // (lanes = rows then write distinct 16-byte chunks: conflict-free staging)
+  bool inner_cols = true;
+  for (int li : ord) if (legs[li].tdim == 0 && legs[li].kind != 1 && legs[li].dim > 1) inner_cols = false;
+  p.o_swz = (inner_cols && dims[0].box == 16) ? 1 : 0;
+  cuuint64_t gdim[5], gstr[4];
+  cuuint32_t box[5], estr[5];
+  for (size_t k = 0; k < dims.size(); ++k) {
+    gdim[k] = (cuuint64_t)dims[k].ext;
+    box[k] = (cuuint32_t)dims[k].box;
+    estr[k] = 1;
+    if (k) gstr[k - 1] = (cuuint64_t)(dims[k].stride * 8);
+  }
+  if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)dims.size(), d.out, gdim, gstr, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, p.o_swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+          CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  p.o_rank = (int32_t)dims.size();
+  p.tma_out = 1;
+  return true;
 }
 
 // TNC_TC16=0 keeps complex64 GEMM steps on 3xTF32 even when amax_in is given
@@ -716,11 +919,13 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
     const size_t budget = 226 * 1024;
     p.cn_smem = (!d.c_rows_contig && d.N <= 1024 && d.out_zstride < 0x7fffffffLL) ? 1 : 0;
     const int64_t cn = p.cn_smem ? d.N : 0;
-    while (RS + 1 <= TG_MAX_RS && tg_smem_bytes(p.NT, KC, RS + 1, BS, f16, cn) <= budget) ++RS;
-    while (BS + 1 <= TG_MAX_BS && tg_smem_bytes(p.NT, KC, RS, BS + 1, f16, cn) <= budget) ++BS;
+    CUtensorMap tmO;
+    const int tma = tg_out_map(d, p, tmO, enc) ? 1 : 0;
+    while (RS + 1 <= TG_MAX_RS && tg_smem_bytes(p.NT, KC, RS + 1, BS, f16, cn, tma) <= budget) ++RS;
+    while (BS + 1 <= TG_MAX_BS && tg_smem_bytes(p.NT, KC, RS, BS + 1, f16, cn, tma) <= budget) ++BS;
     if (const char* e = getenv("TNC_TG_RS")) RS = atoi(e);
     if (const char* e = getenv("TNC_TG_BS")) BS = atoi(e);
-    if (tg_smem_bytes(p.NT, KC, RS, BS, f16, cn) > budget) return 0;
+    if (tg_smem_bytes(p.NT, KC, RS, BS, f16, cn, tma) > budget) return 0;
     p.RS = RS; p.BS = BS;
     // A: [Z][M][2K floats] with row pitch K complex, batch pitch acc_zstride complex
     CUtensorMap tm;
@@ -774,7 +979,7 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
     p.items = p.Z * p.tiles_m * p.tiles_n;
     p.per_cta = (p.items + sms - 1) / sms;
     const int64_t grid = (p.items + p.per_cta - 1) / p.per_cta;
-    const size_t smem = tg_smem_bytes(p.NT, KC, RS, BS, f16, cn);
+    const size_t smem = tg_smem_bytes(p.NT, KC, RS, BS, f16, cn, tma);
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(k_tc_gemm<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -782,9 +987,10 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
       cudaFuncSetAttribute(k_tc_gemm<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       attr = true;
     }
-    if (f16) k_tc_gemm<16, true><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm);
-    else if (KC == 16) k_tc_gemm<16, false><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm);
-    else k_tc_gemm<8, false><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm);
+    const CUtensorMap& to = tma ? tmO : tm;
+    if (f16) k_tc_gemm<16, true><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm, to);
+    else if (KC == 16) k_tc_gemm<16, false><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm, to);
+    else k_tc_gemm<8, false><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm, to);
     const bool ok = cudaGetLastError() == cudaSuccess;
     cudaFreeAsync(bp, s);
     return ok ? 1 : -1;

@@ -132,6 +132,8 @@ class StepPlan:
     f_cstride: list = field(default_factory=list)
     c_noff: np.ndarray = None
     site_layout: list = None  # [cut legs..., shared..., new...]
+    n_dim: list = field(default_factory=list)      # new legs (site order, merged), result strides
+    n_cstride: list = field(default_factory=list)
 
 
 class ContractionPlan:
@@ -198,11 +200,13 @@ class ContractionPlan:
             ostr = dict(zip(out, _strides(odims)))
             c_contig = out == free + new_out
             fd, fa, fc = _merge_rows([ext[e] for e in free], [astr[e] for e in free], [ostr[e] for e in free])
+            nd_, _, nc_ = _merge_rows([ext[e] for e in new_out], [ostr[e] for e in new_out], [ostr[e] for e in new_out])
             sp = StepPlan(
                 node=q, acc_legs=list(acc), shared=shared, free=free, new=new_out, out_legs=out,
                 M=M, K=K, N=N, c_rows_contig=c_contig, f_dim=fd, f_astride=fa, f_cstride=fc,
                 c_noff=_mixed([ext[e] for e in new_out], [ostr[e] for e in new_out]),
                 site_layout=[e for e in self.cut if e in set(spec.legs[q])] + shared + new_out,
+                n_dim=nd_, n_cstride=nc_,
             )
             if len(fd) > NV.MAX_LEGS:
                 raise EngineError(f"step {t}: {len(fd)} free legs exceed TNC_MAX_LEGS")
@@ -375,6 +379,10 @@ class PathExecutor:
             d.a_rows_contig = 1
             d.c_rows_contig = 1 if sp.c_rows_contig else 0
             d.c_n_contig = 1 if np.array_equal(sp.c_noff, np.arange(sp.N)) else 0
+            d.nn = len(sp.n_dim) if len(sp.n_dim) <= NV.MAX_LEGS else 0
+            for j in range(d.nn):
+                d.n_dim[j] = sp.n_dim[j]
+                d.n_cstride[j] = sp.n_cstride[j]
             d.b_dense = 1
             d.conj_b = 0
         # complex64 tensor-core GEMM steps take their input's per-z magnitude

@@ -1,7 +1,12 @@
-"""Tensor-core (tcgen05 3xTF32) contraction path vs the CPU oracle."""
+"""Tensor-core (tcgen05 3xTF32 / fp16-split) contraction paths and the SIMT
+step kernels vs the CPU oracle and complex128 references."""
+
+from pathlib import Path
 
 import numpy as np
 import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
 
 import tn_oracle as O
 
@@ -233,3 +238,33 @@ def test_skinny_and_few_row_steps(M, K, N, dtype):
     ref = acc.reshape(Z, M, K).to(torch.complex128) @ site
     err = ((out.reshape(Z, M, N).to(torch.complex128) - ref).norm() / ref.norm()).item()
     assert err <= (2e-6 if dtype == "complex64" else 1e-13), err
+
+
+def test_tma_store_epilogue_matches():
+    """The opt-in TMA-store epilogue (TNC_TG_TMAOUT=1) writes the same
+    amplitudes as the default register/LSU epilogue on a 53-qubit network
+    with interleaved result layouts (subprocess: the switch is read once)."""
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, '.');"
+        "from paper_2011_02621_b200 import AmplitudeEngine, pattern_rqc, sycamore53_graph;"
+        "g, pats, _ = sycamore53_graph();"
+        "c = pattern_rqc(g, [pats[ch] for ch in 'ABCDCDAB'], 6, seed=12);"
+        "rng = np.random.default_rng(3);"
+        "outs = [''.join(rng.choice(['0', '1'], 53)) for _ in range(4)];"
+        "a = AmplitudeEngine(c, dtype='complex64', max_rank=10).amplitudes(outs);"
+        "np.save(sys.argv[1], a)"
+    )
+    import os
+    import tempfile
+
+    res = []
+    with tempfile.TemporaryDirectory() as td:
+        for flag in ("0", "1"):
+            f = os.path.join(td, f"a{flag}.npy")
+            env = dict(os.environ, TNC_TG_TMAOUT=flag)
+            subprocess.run([sys.executable, "-c", code, f], check=True, env=env, cwd=str(ROOT))
+            res.append(np.load(f))
+    assert rel_l2(res[1], res[0]) <= 1e-6
