@@ -44,6 +44,7 @@ namespace tnc {
 struct GemmDesc {
   int64_t Z, M, K, N;
   int64_t tiles_m, per_cta, items;
+  int32_t ilv, _pad5;            // 1: row tiles dealt round-robin over CTAs (neighbouring CTAs on neighbouring tiles)
   int32_t NT, tiles_n;           // complex columns per N tile (multiple of 16)
   int32_t KC, nchunk;            // complex K per chunk
   int32_t RS, BS;                // raw A stages, B stages
@@ -301,13 +302,22 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
   if (p.cn_smem)
     for (int n = threadIdx.x; n < p.N; n += blockDim.x) cn_s[n] = (int32_t)p.c_noff[n];
 
-  const int64_t w0 = blockIdx.x * p.per_cta;
-  const int64_t w1 = min(w0 + p.per_cta, p.items);
-  const int nitems = (int)(w1 - w0);
+  // items of this CTA: a contiguous range (ilv = 0), or whole row tiles
+  // (groups of tiles_n items) dealt round-robin, so that at any moment the
+  // CTAs stream neighbouring rows of A and of the result (DRAM page locality)
+  const int64_t G = p.Z * p.tiles_m;
+  const int64_t w0 = p.ilv ? 0 : blockIdx.x * p.per_cta;
+  const int nitems = p.ilv ? (int)(((G - blockIdx.x + gridDim.x - 1) / gridDim.x) * p.tiles_n)
+                           : (int)(min(w0 + p.per_cta, p.items) - w0);
+  auto itemw = [&](int it) -> int64_t {
+    if (!p.ilv) return w0 + it;
+    const int g = it / p.tiles_n;
+    return ((int64_t)g * gridDim.x + blockIdx.x) * p.tiles_n + (it - g * p.tiles_n);
+  };
   const int64_t per_z = p.tiles_m * p.tiles_n;
   // ares groups: consecutive items of one row tile (column tile index = w % tiles_n)
-  auto gstart = [&](int it) { return it == 0 || (w0 + it) % p.tiles_n == 0; };
-  auto gend = [&](int it) { return it == nitems - 1 || (w0 + it) % p.tiles_n == p.tiles_n - 1; };
+  auto gstart = [&](int it) { return it == 0 || itemw(it) % p.tiles_n == 0; };
+  auto gend = [&](int it) { return it == nitems - 1 || itemw(it) % p.tiles_n == p.tiles_n - 1; };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < RS; ++s) { mbar_init(&rfull[s], 1); mbar_init(&rempty[s], CONVW); }
@@ -341,7 +351,7 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
     for (int it = 0; it < nitems; ++it) {
       if (ares && !gstart(it)) continue;
       if constexpr (F16) {
-        const int64_t zz = (w0 + it) / per_z;
+        const int64_t zz = itemw(it) / per_z;
         if (zz != sz) { sz = zz; sA = f16_scale(__ldg(p.amax_in + zz)); }
       }
       for (int c = 0; c < nchunk; ++c, ++j) {
@@ -432,7 +442,7 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
       const uint32_t ph = (it / TS) & 1;
       int64_t z, mt, nt;
       {
-        const int64_t w = w0 + it;
+        const int64_t w = itemw(it);
         if (p.items < 0x7fffffffLL) {
           const uint32_t w32 = (uint32_t)w, pz = (uint32_t)per_z, tn = (uint32_t)p.tiles_n;
           const uint32_t z32 = w32 / pz, rem = w32 - z32 * pz, m32 = rem / tn;
@@ -668,7 +678,7 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
     uint32_t rph = 0;
     for (int it = 0; it < nitems; ++it) {
       if (ares && !gstart(it)) continue;
-      const int64_t w = w0 + it;
+      const int64_t w = itemw(it);
       const int64_t z = w / per_z;
       const int64_t mt = (w - z * per_z) / p.tiles_n;
       for (int c = 0; c < nchunk; ++c, ++j) {
@@ -683,7 +693,7 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
     int bi = 0, bs = 0;
     uint32_t bph = 0;
     for (int it = 0; it < nitems; ++it) {
-      const int64_t w = w0 + it;
+      const int64_t w = itemw(it);
       const int64_t z = w / per_z;
       const int64_t nt = (w - z * per_z) % p.tiles_n;
       const unsigned char* src = p.bp + gemm_combo(p, z) * p.bp_combo_stride + (int64_t)nt * nchunk * 6 * bbytes;
@@ -978,7 +988,9 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     p.items = p.Z * p.tiles_m * p.tiles_n;
     p.per_cta = (p.items + sms - 1) / sms;
-    const int64_t grid = (p.items + p.per_cta - 1) / p.per_cta;
+    p.ilv = 0;                     // round-robin tiles (TNC_TG_ILV=1) measured neutral
+    if (const char* e = getenv("TNC_TG_ILV")) p.ilv = atoi(e);
+    const int64_t grid = p.ilv ? std::min<int64_t>(sms, p.Z * p.tiles_m) : (p.items + p.per_cta - 1) / p.per_cta;
     const size_t smem = tg_smem_bytes(p.NT, KC, RS, BS, f16, cn, tma);
     static bool attr = false;
     if (!attr) {
