@@ -18,6 +18,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <cuda_fp16.h>
 #include "tnc_common.cuh"
 
 namespace tnc {
@@ -41,8 +42,9 @@ struct TcDesc {
   int32_t rows_contig;             // lo_off[r] = r*K and akoff[k] = k (tables unused)
   int32_t nstages;                 // A-chunk ring depth (host: as many as fit)
   int32_t dbg;                     // experiment flags (0 in production): 1 no stores, 2 no loads, 4 no MMA
-  int32_t _pad2;
+  int32_t f16;                     // 1: fp16-split operands, per-row A scales, per-z site scales (bscale)
   unsigned long long* trace;       // dbg & 128: per-tile globaltimer stamps of CTA 0
+  const float* bscale;             // [Z] max |re|,|im| of the site block of z (f16)
   // raw-ring mode: each tile's 128 x K accumulator block is staged by cp.async.bulk
   // as Kout contiguous segments of Lseg elements; element (r, k) sits at
   // lo_off[r] + kraw[k] inside the staged tile
@@ -150,14 +152,74 @@ __host__ __device__ inline int64_t tc_smem_bytes(int64_t K, int64_t N, int64_t p
          + TC_EPI_WARPS * 32 * TC_EPI_PITCH + 16 + rs * tc_raw_bytes(K);
 }
 // TMEM plan: TS accumulators of Nr columns, AS A-chunk stages of 4*KC columns (hi + lo)
-__host__ __device__ inline void tc_tmem_plan(int64_t K, int64_t N, int& TS, int& AS) {
+// f16: A stages of 2*kc columns (two fp16 per column) and TS columns at the
+// top of TMEM for the per-row inverse scales of each accumulator stage
+__host__ __device__ inline void tc_tmem_plan(int64_t K, int64_t N, int& TS, int& AS, bool f16 = false) {
   const int Nr = (int)(2 * N), kc = (int)tc_kc(K);
   TS = 256 / Nr;
   if (TS > TC_MAX_STAGES) TS = TC_MAX_STAGES;
   TS &= ~1;                                     // even: each epilogue group owns its stages
   if (TS < 2) TS = 2;
-  AS = (512 - TS * Nr) / (4 * kc);
+  AS = f16 ? (512 - TS * Nr - TS) / (2 * kc) : (512 - TS * Nr) / (4 * kc);
   if (AS > TC_MAX_STAGES) AS = TC_MAX_STAGES;
+}
+
+// power-of-two scale s with max * s in [2^14, 2^15) (1 for zero / non-finite)
+__host__ __device__ inline float tc_f16_scale(float amax) {
+  if (!(amax > 0.f) || !(amax < 3.0e38f)) return 1.f;
+  int e;
+#ifdef __CUDA_ARCH__
+  e = (int)((__float_as_uint(amax) >> 23) & 0xff) - 127;
+#else
+  uint32_t u;
+  memcpy(&u, &amax, 4);
+  e = (int)((u >> 23) & 0xff) - 127;
+#endif
+  int pw = 14 - e;
+  pw = pw < -126 ? -126 : (pw > 127 ? 127 : pw);
+#ifdef __CUDA_ARCH__
+  return __uint_as_float((uint32_t)(pw + 127) << 23);
+#else
+  const uint32_t b = (uint32_t)(pw + 127) << 23;
+  float f;
+  memcpy(&f, &b, 4);
+  return f;
+#endif
+}
+// y0, y1 -> packed fp16 hi and lo (low half = y0); see tnc_tcgemm.cuh split_f16x2
+__device__ __forceinline__ void tc_split_f16x2(float y0, float y1, uint32_t& h, uint32_t& l) {
+  const float h0 = __uint_as_float((__float_as_uint(y0) + 0x1000u) & 0xFFFFE000u);
+  const float h1 = __uint_as_float((__float_as_uint(y1) + 0x1000u) & 0xFFFFE000u);
+  const float l0 = y0 - h0, l1 = y1 - h1;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(h1), "f"(h0));
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(l) : "f"(l1), "f"(l0));
+}
+__device__ __forceinline__ void tc_split_f16(float y, uint16_t& h, uint16_t& l) {
+  const __half hh = __float2half_rn(y);
+  const __half ll = __float2half_rn(y - __half2float(hh));
+  h = __half_as_ushort(hh);
+  l = __half_as_ushort(ll);
+}
+// per batch element z: max |re|, |im| over its site block (f16 scale of B')
+__global__ void k_tc_bmax(const __grid_constant__ TcDesc p, float* out) {
+  for (int64_t z = blockIdx.x; z < p.Z; z += gridDim.x) {
+    const float2* S = reinterpret_cast<const float2*>(p.site.ptr) + site_offset(p.site, z, p.slices_per_b, p.s0);
+    float m = 0.f;
+    for (int64_t e = threadIdx.x; e < p.K * p.N; e += blockDim.x) {
+      const int64_t k = e / p.N, n = e - k * p.N;
+      const float2 v = __ldg(S + p.b_koff[k] + p.b_noff[n]);
+      m = fmaxf(m, fmaxf(fabsf(v.x), fabsf(v.y)));
+    }
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    __shared__ float red[32];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, red[w]);
+      out[z] = m;
+    }
+    __syncthreads();
+  }
 }
 
 __device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
@@ -166,6 +228,14 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, ui
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}"
+      ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_f16_tc(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
       ::"r"(d_tmem), "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
 template <int NW, int LEN>
@@ -193,16 +263,32 @@ __device__ __forceinline__ void tmem_st(uint32_t taddr, const uint32_t (&v)[LEN]
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // B' (hi, lo) for batch element z, written by threads [tid0, tid0 + nthr)
+template <bool F16>
 __device__ __forceinline__ void build_b(const TcDesc& p, int64_t z, float* Bhi, float* Blo, int tid, int nthr) {
   const int K = (int)p.K, N = (int)p.N;
   const uint32_t SBO_B = ((2 * K) / 4) * 128;
   const float2* S = reinterpret_cast<const float2*>(p.site.ptr) + site_offset(p.site, z, p.slices_per_b, p.s0);
+  const float t = F16 ? tc_f16_scale(__ldg(p.bscale + z)) : 1.f;
   for (int e = tid; e < K * N; e += nthr) {
     const int k = e / N, n = e - (e / N) * N;
     float2 sv = __ldg(S + p.b_koff[k] + p.b_noff[n]);
     if (p.conj_b) sv.y = -sv.y;
     // rows n' = 2n (re out), 2n+1 (im out); cols k' = 2k (re in), 2k+1 (im in)
     const float vals[4] = {sv.x, -sv.y, sv.y, sv.x};
+    if constexpr (F16) {
+      // 16-bit K-major canonical: 8 rows x 16 B core matrices, LBO 128 B along K, SBO (2K/8)*128 B along N
+      const uint32_t SBO16 = ((2 * K) / 8) * 128;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int nr = 2 * n + (q >> 1), kr = 2 * k + (q & 1);
+        const uint32_t off = (nr & 7) * 16 + (nr >> 3) * SBO16 + (kr >> 3) * 128 + (kr & 7) * 2;
+        uint16_t h, l;
+        tc_split_f16(vals[q] * t, h, l);
+        *reinterpret_cast<uint16_t*>(reinterpret_cast<unsigned char*>(Bhi) + off) = h;
+        *reinterpret_cast<uint16_t*>(reinterpret_cast<unsigned char*>(Blo) + off) = l;
+      }
+      continue;
+    }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int nr = 2 * n + (q >> 1), kr = 2 * k + (q & 1);
@@ -216,9 +302,10 @@ __device__ __forceinline__ void build_b(const TcDesc& p, int64_t z, float* Bhi, 
 }
 
 // KH = complex values per converter thread per chunk (KC / 2)
-template <int KH>
+template <int KH, bool F16>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_tc_c64(const __grid_constant__ TcDesc p) {
+  static_assert(!F16 || KH == 8, "F16 needs 16-complex chunks");
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   constexpr int KC = 2 * KH;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -228,9 +315,11 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
   const int nchunk = K / KC;
   const uint32_t SBO_B = (Kr / 4) * 128;
   int TS, AS;
-  tc_tmem_plan(p.K, Np, TS, AS);
+  tc_tmem_plan(p.K, Np, TS, AS, F16);
   const uint32_t A0 = (uint32_t)(TS * Nr);      // first A column
-  constexpr uint32_t ACOLS = 4 * KC;            // per A stage: hi (2KC) + lo (2KC)
+  // per A stage: tf32 hi (2KC) + lo (2KC) columns; f16 hi (KC) + lo (KC), one complex per column
+  constexpr uint32_t ACOLS = F16 ? 2 * KC : 4 * KC;
+  const uint32_t SCOL = 512u - (uint32_t)TS;    // f16: column SCOL + acc = per-row inverse scales
   // ---- shared memory carve-up ----
   float* Bhi = reinterpret_cast<float*>(smem_raw);
   float* Blo = Bhi + (size_t)Nr * Kr;
@@ -288,7 +377,7 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
     for (int i = threadIdx.x; i < 2 * Nr * Kr / 4; i += blockDim.x) bz[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
   }
-  if (ntiles > 0) build_b(p, z0, Bhi, Blo, threadIdx.x, blockDim.x);
+  if (ntiles > 0) build_b<F16>(p, z0, Bhi, Blo, threadIdx.x, blockDim.x);
   for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
     const int64_t g = g0 + t;
     const int64_t zt = g / p.tiles_per_z;
@@ -334,6 +423,24 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
         raw = reinterpret_cast<const float2*>(rawring + (size_t)rs * tc_raw_bytes(p.K)) + looff_s[r];
       }
       const float2* Ar = A + tbase[t];
+      float sA = 1.f;
+      if constexpr (F16) {
+        // per-row scale from the whole row (the raw stage holds the full 128 x K tile)
+        float m = 0.f;
+        for (int k = 0; k < K; ++k) {
+          const float2 x = raw[kraw_s[k]];
+          m = fmaxf(m, fmaxf(fabsf(x.x), fabsf(x.y)));
+        }
+        sA = tc_f16_scale(m);
+        const float inv = 1.f / sA;              // the site factor 1/t(z) is applied by the epilogue
+        // the accumulator stage's scale column is free once its previous tile is drained
+        const int acc = t % TS;
+        mbar_wait_spin(&tempty[acc], (uint32_t)(((t / TS) & 1) ^ 1));
+        tc_fence_after();
+        uint32_t iv[1] = {__float_as_uint(inv)};
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};"
+                     ::"r"(tmem + lane_base + SCOL + (uint32_t)acc), "r"(iv[0]));
+      }
       for (int c = 0; c < nchunk; ++c, ++j) {
         const int stage = grp * ASg + j % ASg;
         const uint32_t ph = (j / ASg) & 1;
@@ -350,8 +457,15 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
         mbar_wait_spin(&empty[stage], ph ^ 1);
         tc_fence_after();
         const uint32_t col = A0 + (uint32_t)stage * ACOLS;
+        if constexpr (F16) {
+          uint32_t hi[KC], lo[KC];
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
+          for (int q = 0; q < KC; ++q) tc_split_f16x2(v[q].x * sA, v[q].y * sA, hi[q], lo[q]);
+          tmem_st<KC>(tmem + lane_base + col, hi);
+          tmem_st<KC>(tmem + lane_base + col + KC, lo);
+        }
+#pragma unroll
+        for (int half = 0; half < (F16 ? 0 : 2); ++half) {
           uint32_t hi[KC], lo[KC];
 #pragma unroll
           for (int q = 0; q < KC / 2; ++q) {
@@ -398,6 +512,15 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
       const int64_t grow = (gt - zt * p.tiles_per_z) * 128 + r;
       float2* otile = p.out + zt * p.out_zstride + (grow - lane) * N;   // this warp's 32 rows
       const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * Nr);
+      float inv = 1.f, inv2 = 1.f;
+      if constexpr (F16) {
+        inv2 = 1.f / tc_f16_scale(__ldg(p.bscale + zt));
+        uint32_t iv;
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
+                     : "=r"(iv) : "r"(tmem + ((uint32_t)(q * 32) << 16) + SCOL + (uint32_t)acc));
+        tmem_wait_ld();
+        inv = __uint_as_float(iv);
+      }
       for (int c0 = 0; c0 < Nr; c0 += 32) {
         const int cols = (c0 + 32 <= Nr) ? 32 : 16;
         uint32_t v[32];
@@ -417,6 +540,10 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
         if (c0 + 32 >= Nr) {              // accumulator drained: hand it back before the stores
           tc_fence_before();
           mbar_arrive_warp(&tempty[acc]);
+        }
+        if constexpr (F16) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * inv * inv2);
         }
 #pragma unroll
         for (int j = 0; j < 8; ++j)
@@ -445,6 +572,7 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
   } else if (warp == TC_MMA_WARP) {
     // ---------------- MMA issuer (A from TMEM, B from smem) ----------------
     const uint32_t idesc = tf32_idesc(Nr);
+    const uint32_t idesc16 = (1u << 4) | ((uint32_t)(Nr >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
     const uint32_t bhi = smem_u32(Bhi), blo = smem_u32(Blo);
     int it = 0;
     int64_t cur_z = z0;
@@ -466,7 +594,7 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
         mbar_wait(bdone, bdone_phase);
         bdone_phase ^= 1;
         tc_fence_after();
-        build_b(p, zt, Bhi, Blo, lane, 32);
+        build_b<F16>(p, zt, Bhi, Blo, lane, 32);
         fence_proxy_async();
         __syncwarp();
         tc_fence_before();
@@ -485,7 +613,22 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
         mbar_wait_spin(&full[stage], ph);
         TC_TRACE(8, it);
         tc_fence_after();
-        if (lane == 0) {
+        if (F16 && lane == 0) {
+          // chunk c = reals [2KC c, 2KC (c+1)) of K'; per 16-real k-step: one column group of 8
+          const uint32_t SBO16 = (Kr / 8) * 128;
+          const uint32_t ahi = tmem + A0 + (uint32_t)stage * ACOLS, alo = ahi + KC;
+#pragma unroll
+          for (int s = 0; s < KC / 8; ++s) {
+            const uint32_t kb = (uint32_t)((2 * KC * c + 16 * s) / 8) * 128;   // byte offset along K'
+            const uint64_t dbh = umma_desc(bhi + kb, 128, SBO16), dbl = umma_desc(blo + kb, 128, SBO16);
+            const uint32_t first = (c == 0 && s == 0) ? 0u : 1u;
+            mma_f16_tc(d, alo + 8 * s, dbh, idesc16, first);
+            mma_f16_tc(d, ahi + 8 * s, dbl, idesc16, 1u);
+            mma_f16_tc(d, ahi + 8 * s, dbh, idesc16, 1u);
+          }
+          umma_commit(&empty[stage]);
+          if (c == nchunk - 1) umma_commit(&tfull[acc]);
+        } else if (!F16 && lane == 0) {
           const uint32_t ahi = tmem + A0 + (uint32_t)stage * ACOLS, alo = ahi + 2 * KC;
           const uint64_t dbh0 = umma_desc(bhi + (uint32_t)(c * KC / 2) * 128, 128, SBO_B);
           const uint64_t dbl0 = umma_desc(blo + (uint32_t)(c * KC / 2) * 128, 128, SBO_B);
@@ -548,9 +691,10 @@ __host__ inline bool tc_shape_ok(int64_t K, int64_t N, int64_t M) {
 __host__ inline int launch_tc(TcDesc p, int64_t Z, cudaStream_t s) {
   static bool attr_done = false;
   if (!attr_done) {
-    if (cudaFuncSetAttribute(k_tc_c64<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
-        cudaFuncSetAttribute(k_tc_c64<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
-        cudaFuncSetAttribute(k_tc_c64<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
+    if (cudaFuncSetAttribute(k_tc_c64<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
+        cudaFuncSetAttribute(k_tc_c64<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
+        cudaFuncSetAttribute(k_tc_c64<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
+        cudaFuncSetAttribute(k_tc_c64<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
       return -1;
     attr_done = true;
   }
@@ -587,9 +731,24 @@ __host__ inline int launch_tc(TcDesc p, int64_t Z, cudaStream_t s) {
     cudaMemset(p.trace, 0, 18 * 64 * sizeof(unsigned long long));
   }
   const int kc = (int)tc_kc(p.K);
-  if (kc == 4) k_tc_c64<2><<<(unsigned)grid, TC_THREADS, smem, s>>>(p);
-  else if (kc == 8) k_tc_c64<4><<<(unsigned)grid, TC_THREADS, smem, s>>>(p);
-  else k_tc_c64<8><<<(unsigned)grid, TC_THREADS, smem, s>>>(p);
+  // fp16-split operands (per-row A scales, per-z site scales) when the raw
+  // ring holds whole tiles and the chunks are 16 complex (kind::f16 K = 16)
+  int TS16, AS16;
+  tc_tmem_plan(p.K, tc_npad(p.N), TS16, AS16, true);
+  const char* e16 = getenv("TNC_TC16");
+  // (K = 16 only: with several chunks per tile the per-row scale needs an extra
+  // pass over the staged tile, which measured slower than 3xTF32 at K = 64)
+  p.f16 = (kc == 16 && p.K == 16 && p.raw_stages > 0 && AS16 >= 2 && !(e16 && e16[0] == '0')) ? 1 : 0;
+  float* bsc = nullptr;
+  if (p.f16) {
+    if (cudaMallocAsync(reinterpret_cast<void**>(&bsc), (size_t)Z * sizeof(float), s) != cudaSuccess) return -1;
+    p.bscale = bsc;
+    k_tc_bmax<<<(unsigned)std::min<int64_t>(Z, 4096), 128, 0, s>>>(p, bsc);
+    k_tc_c64<8, true><<<(unsigned)grid, TC_THREADS, smem, s>>>(p);
+    cudaFreeAsync(bsc, s);
+  } else if (kc == 4) k_tc_c64<2, false><<<(unsigned)grid, TC_THREADS, smem, s>>>(p);
+  else if (kc == 8) k_tc_c64<4, false><<<(unsigned)grid, TC_THREADS, smem, s>>>(p);
+  else k_tc_c64<8, false><<<(unsigned)grid, TC_THREADS, smem, s>>>(p);
   if (p.dbg & 128) {
     unsigned long long h[18 * 64];
     cudaStreamSynchronize(s);

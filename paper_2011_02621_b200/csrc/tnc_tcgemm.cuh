@@ -432,7 +432,7 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
     // innermost result leg is a free leg: consecutive rows are contiguous)
     const bool staged = p.c_rows_contig || p.n_contig || (p.N > 1 && p.c_noff[1] == p.c_noff[0] + 1);
     const int cfirst = alt ? 0 : eg * 16, cstep = alt ? 16 : 16 * EPIG;
-    float inv = 1.f;
+    float inv = 1.f, inv2 = 1.f;
     int64_t inv_z = -1;
     const uint32_t stg_s = smem_u32(stg);
     const uint32_t ostage_s = smem_u32(estage);
@@ -470,7 +470,10 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
       if constexpr (F16) {
         if (z != inv_z) {                        // the per-z scales change rarely: reload only then
           inv_z = z;
-          inv = 1.f / (f16_scale(__ldg(p.amax_in + z)) * f16_scale(__ldg(p.bscale + gemm_combo(p, z))));
+          // two exact power-of-two factors: their product can leave the fp32 range
+          // when both tensors are tiny although every result is representable
+          inv = 1.f / f16_scale(__ldg(p.amax_in + z));
+          inv2 = 1.f / f16_scale(__ldg(p.bscale + gemm_combo(p, z)));
         }
       }
       mbar_wait(&tfull[acc], ph);
@@ -493,7 +496,7 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
         }
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj) {
-          const float a = __uint_as_float(vr[jj]) * inv, b = __uint_as_float(vi[jj]) * inv;
+          const float a = __uint_as_float(vr[jj]) * inv * inv2, b = __uint_as_float(vi[jj]) * inv * inv2;
           vmax = fmaxf(vmax, fmaxf(fabsf(a), fabsf(b)));
           vr[jj] = __float_as_uint(a);
           vi[jj] = __float_as_uint(b);

@@ -17,9 +17,13 @@ def rel_l2(got, ref):
     return float(np.linalg.norm(np.asarray(got) - ref) / np.linalg.norm(ref))
 
 
-@pytest.mark.parametrize("r,k,n,B", [(7, 1, 2, 2), (7, 2, 2, 3), (8, 3, 3, 2), (9, 1, 3, 2), (9, 3, 2, 3),
-                                     (10, 2, 3, 1), (11, 3, 3, 1), (7, 3, 2, 1), (8, 3, 1, 3), (9, 3, 1, 1)])
-def test_tc_pair_matches_oracle(r, k, n, B):
+@pytest.mark.parametrize("r,k,n,B,ascale,bscale", [
+    (7, 1, 2, 2, 1.0, 1.0), (7, 2, 2, 3, 1.0, 1.0), (8, 3, 3, 2, 1.0, 1.0), (9, 1, 3, 2, 1.0, 1.0),
+    (9, 3, 2, 3, 1.0, 1.0), (10, 2, 3, 1, 1.0, 1.0), (11, 3, 3, 1, 1.0, 1.0), (7, 3, 2, 1, 1.0, 1.0),
+    (8, 3, 1, 3, 1.0, 1.0), (9, 3, 1, 1, 1.0, 1.0),
+    # fp16-split path: arbitrary operand scales and a wide per-row dynamic range
+    (9, 2, 2, 3, 1e-25, 1e20), (8, 3, 2, 2, 3e12, 1e-9), (10, 2, 3, 2, 1e-22, 1e-8), (8, 3, 3, 2, 7e-3, 5e4)])
+def test_tc_pair_matches_oracle(r, k, n, B, ascale, bscale):
     import torch
 
     from paper_2011_02621_b200.engine import PairPlan
@@ -28,9 +32,12 @@ def test_tc_pair_matches_oracle(r, k, n, B):
     perm = list(rng.permutation(r + k))
     dims = [2 if x < r else 4 for x in perm]
     size = int(np.prod(dims))
-    acc = ((rng.standard_normal((B, size)) + 1j * rng.standard_normal((B, size))) / np.sqrt(2)).astype(np.complex64)
+    acc = ((rng.standard_normal((B, size)) + 1j * rng.standard_normal((B, size))) / np.sqrt(2))
+    if ascale != 1.0:
+        acc = acc * np.exp(rng.uniform(-6, 6, (B, size)))      # rows spanning ~5 decades
+    acc = (acc * ascale).astype(np.complex64)
     site = ((rng.standard_normal((2,) + (4,) * (k + n)) + 1j * rng.standard_normal((2,) + (4,) * (k + n))) / 2
-            ).astype(np.complex64)
+            * bscale).astype(np.complex64)
     bits = rng.integers(0, 2, B)
     shared_pos = sorted((i for i, x in enumerate(perm) if x >= r), key=lambda i: perm[i])
     pairs = [(p, j) for j, p in enumerate(shared_pos)]
@@ -150,9 +157,12 @@ def test_tc_gemm_scaled_precision(M, K, N):
     assert abs(got - ref) / abs(scale) <= 2e-7
 
 
-@pytest.mark.parametrize("M,K,N,scale", [(8192, 128, 256, 1.0), (16384, 256, 128, 3e-21), (8192, 16, 128, 7e12),
-                                         (32768, 16, 16, 1.0), (8192, 64, 24, 1e-3)])
-def test_tc_gemm_f16_split_step(M, K, N, scale):
+@pytest.mark.parametrize("M,K,N,scale,sscale", [(8192, 128, 256, 1.0, 1.0), (16384, 256, 128, 3e-21, 1.0),
+                                                 (8192, 16, 128, 7e12, 1.0), (32768, 16, 16, 1.0, 1.0),
+                                                 (8192, 64, 24, 1e-3, 1.0),
+                                                 # both scales large: their product leaves the fp32 range
+                                                 (8192, 128, 256, 1e-25, 1e-12), (16384, 16, 16, 1e-24, 1e-13)])
+def test_tc_gemm_f16_split_step(M, K, N, scale, sscale):
     """fp16-split tcgen05 GEMM (a step given amax_in): one step acc[M, K] x
     S[K, N] on inputs spanning ~12 decades around an arbitrary overall scale
     matches the complex128 product to the 3xTF32 level (relative L2 <= 2e-6),
@@ -170,6 +180,7 @@ def test_tc_gemm_f16_split_step(M, K, N, scale):
     g = torch.Generator(device="cuda")
     g.manual_seed(M + K + N)
     sites = {q: torch.randn((1,) + spec.site_dims(q), dtype=torch.complex64, device="cuda", generator=g) for q in range(3)}
+    sites[1] = sites[1] * sscale
     plan = ContractionPlan(spec, [0, 1, 2])
     sp = plan.steps[0]
     assert (sp.M, sp.K, sp.N) == (M, K, N)

@@ -18,7 +18,8 @@ tot = sum(float(r[i_s] or 0) for r in data) or 1.0
 waits = defaultdict(float)
 for r in data:
     if "TRYWAIT" in r[i_src]:
-        bar = r[i_src].split("[")[1].split("]")[0].split("+")[-1]
+        inner = r[i_src].split("[")[1].split("]")[0]
+        bar = inner.split("+")[-1] if "+0x" in inner else "0x0(" + inner + ")"
         waits[bar] += float(r[i_ex] or 0)
 print("mbarrier try_wait executions by barrier offset:")
 for k, v in sorted(waits.items(), key=lambda x: -x[1]):
