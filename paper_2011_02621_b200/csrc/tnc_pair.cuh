@@ -241,7 +241,7 @@ k_pair_pipe(const __grid_constant__ PairTile p, const void* __restrict__ A_, con
       __syncthreads();
       cur_z = z;
     }
-    mbar_wait(&bars[stage], phase);
+    mbar_wait_spin(&bars[stage], phase);
     const C* tile = ring + stage * tile_elems;
     C* Ot = O + z * p.out_zstride + u * p.R * p.N;
     for (int64_t r = threadIdx.x; r < p.R; r += blockDim.x) {
@@ -360,7 +360,7 @@ k_pair_pipe_cols(const __grid_constant__ PairTile p, const void* __restrict__ A_
       }
       cur_z = z;
     }
-    mbar_wait(&bars[stage], phase);
+    mbar_wait_spin(&bars[stage], phase);
     const C* tile = ring + stage * tile_elems;
     C* Ot = O + z * p.out_zstride + u * p.R * p.N;
     for (int row = row0; row < Rr; row += row_step) {
