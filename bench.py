@@ -473,14 +473,14 @@ def run_cfg0(args, rank, world, dev):
     amp = torch.zeros(B, dtype=torch.complex128, device=dev)
     stream = torch.cuda.current_stream(dev)
     for _ in range(args.warmup):
-        eng.amplitudes_device(sel, B, amp)
+        eng.amplitudes_device(sel, B, amp, graph=True)
     barrier(world)
     torch.cuda.synchronize(dev)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev.index) as clk:
         e0.record(stream)
         for _ in range(args.steps):
-            eng.amplitudes_device(sel, B, amp)
+            eng.amplitudes_device(sel, B, amp, graph=True)
         e1.record(stream)
         torch.cuda.synchronize(dev)
     t = allreduce_max(e0.elapsed_time(e1) * 1e-3, world, dev)
@@ -494,7 +494,8 @@ def run_cfg0(args, rank, world, dev):
     return {"value": world * B * args.steps / t, "unit": "amplitudes/s", "ms_per_step": 1e3 * t / args.steps,
             "gpu_launches": eng.executor.launches_per_chunk() * args.steps,
             "roofline": {"bound": "latency", "achieved": None, "peak": hbm, "unit": "GB/s", "frac": None,
-                         "traffic": None, "note": "9-qubit network: launch-bound, see sweep workload"},
+                         "traffic": None, "note": "9-qubit network: launch-bound; every pass replays one "
+                                                  "CUDA graph of the whole path (projection, steps, slice sum)"},
             "config": {"workload": "configs[0] 3x3 square, 8 cycles, 64 bitstrings", "dtype": "complex128",
                        "l2": "inputs L2-resident (tiny network)"},
             "clocks": clk.summary(), "dtype": "complex128",

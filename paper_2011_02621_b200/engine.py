@@ -338,6 +338,8 @@ class PathExecutor:
             max_batch_elems = max(1, int(0.35 * free) // (2 * self.itemsize * plan.max_elems))
         self.max_z = max(1, int(max_batch_elems))
         self._buf = None
+        self._graphs: dict = {}
+        self._graph_seen: set = set()
         self._build_descs()
 
     def _build_descs(self):
@@ -426,13 +428,16 @@ class PathExecutor:
         return out
 
     def run(self, sel, B: int, amp, slices: range | None = None, stream=None, accumulate=False,
-            b_offset: int = 0):
+            b_offset: int = 0, graph: bool = False):
         """Contract bitstrings [b_offset, b_offset + B) x ``slices``; writes (or
         adds, ``accumulate``) into ``amp[b_offset:b_offset + B]``.
 
         sel: dict node -> device int32 tensor of variant indices over the whole
         batch (None for single-variant sites); amp: device tensor of the engine
-        dtype.
+        dtype.  ``graph``: replay each chunk's launch sequence (projection, every
+        step, slice sum) from a CUDA graph captured on the second call with the
+        same buffers -- the path's launches then cost one graph launch (small,
+        launch-bound networks such as configs[0]).
         """
         torch = self.torch
         plan = self.plan
@@ -446,6 +451,16 @@ class PathExecutor:
         q0 = plan.path[0]
         for ci, (b0, nb, s0, ns) in enumerate(self.chunks(B, slices)):
             b0 += b_offset
+            key = None
+            if graph:
+                acc_flag = 1 if (accumulate or s0 != slices.start) else 0
+                key = (b0, nb, s0, ns, acc_flag, amp.data_ptr(),
+                       tuple(self._selptr(sel, q, b0) for q in plan.path))
+                g = self._graphs.get(key)
+                if g is not None:                  # replay: the descriptors are baked in
+                    with torch.cuda.stream(st):
+                        g.replay()
+                    continue
             z = nb * ns
             bufa, bufb = self._buffers(z)
             cur, nxt = bufa, bufb
@@ -470,6 +485,19 @@ class PathExecutor:
             r.x = cur.data_ptr()
             r.x_zstride = 1
             r.amp = amp.data_ptr() + b0 * self.itemsize
+            if graph:
+                if key in self._graph_seen:
+                    # capture on a side stream; the eager first call already set
+                    # kernel attributes and warmed the allocator
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g):
+                        cs = torch.cuda.current_stream(self.device)
+                        NV.check(L.tnc_contract_path(C.byref(pd), C.c_void_p(cs.cuda_stream)), "tnc_contract_path")
+                    self._graphs[key] = g
+                    with torch.cuda.stream(st):
+                        g.replay()
+                    continue
+                self._graph_seen.add(key)
             NV.check(L.tnc_contract_path(C.byref(pd), sptr), "tnc_contract_path")
         return amp
 

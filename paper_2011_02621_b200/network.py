@@ -419,6 +419,7 @@ class AmplitudeEngine:
         self.sites = self._projected_sites(phi, fused, legs)
         self.executor = PathExecutor(self.plan, self.sites, dtype=dtype, device=self.device,
                                      max_batch_elems=max_batch_elems)
+        self._io: dict = {}
 
     def _projected_sites(self, phi, fused, legs):
         """V_q[o] = sum_s u_q[o, s] A_q[s, ...] with u_q the trailing 2x2 of q
@@ -446,19 +447,41 @@ class AmplitudeEngine:
         t = torch.from_numpy(np.ascontiguousarray(bits.T)).to(self.device)
         return {q: t[q] for q in range(bits.shape[1])}
 
-    def amplitudes_device(self, sel, B: int, amp=None, slices=None):
+    def amplitudes_device(self, sel, B: int, amp=None, slices=None, graph: bool = False):
         import torch
 
         if amp is None:
             amp = torch.zeros(B, dtype=self.executor.tdtype, device=self.device)
-        self.executor.run(sel, B, amp, slices=slices)
+        self.executor.run(sel, B, amp, slices=slices, graph=graph)
         return amp
 
-    def amplitudes(self, bitstrings: Sequence[str], slices=None) -> np.ndarray:
+    def amplitudes(self, bitstrings: Sequence[str], slices=None, graph: bool = True) -> np.ndarray:
+        """Host bitstrings in, host complex128 amplitudes out.  Per batch size
+        the engine keeps pinned staging + device selector/amplitude buffers, so
+        repeated batches replay one CUDA graph per chunk (``graph``)."""
+        import torch
+
         bits = _bits_matrix(bitstrings, self.circuit.num_qubits)
-        sel = self.selectors(bits)
-        amp = self.amplitudes_device(sel, len(bitstrings), slices=slices)
-        return amp.cpu().numpy().astype(np.complex128)
+        B = len(bitstrings)
+        if not graph or slices is not None:
+            sel = self.selectors(bits)
+            amp = self.amplitudes_device(sel, B, slices=slices)
+            return amp.cpu().numpy().astype(np.complex128)
+        bufs = self._io.get(B)
+        if bufs is None:
+            n = self.circuit.num_qubits
+            host_bits = torch.empty((n, B), dtype=torch.int32, pin_memory=True)
+            dev_bits = torch.empty((n, B), dtype=torch.int32, device=self.device)
+            amp = torch.empty(B, dtype=self.executor.tdtype, device=self.device)
+            host_amp = torch.empty(B, dtype=self.executor.tdtype, pin_memory=True)
+            bufs = self._io[B] = (host_bits, dev_bits, {q: dev_bits[q] for q in range(n)}, amp, host_amp)
+        host_bits, dev_bits, sel, amp, host_amp = bufs
+        host_bits.numpy()[...] = bits.T
+        dev_bits.copy_(host_bits, non_blocking=True)
+        self.executor.run(sel, B, amp, graph=True)
+        host_amp.copy_(amp, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        return host_amp.numpy().astype(np.complex128)
 
     @property
     def multiplies(self) -> int:

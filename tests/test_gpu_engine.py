@@ -250,3 +250,33 @@ def test_sharded_ranks_sum_to_full(golden_amplitudes):
             run_sharded(eng.executor, sel, 5, part, rank, world)
             total += part
         assert rel_l2(total.cpu().numpy(), ref) <= 1e-12
+
+
+def test_graph_replay_matches_eager(golden_amplitudes):
+    """CUDA-graph replay of whole path chunks gives the eager amplitudes, also
+    after the inputs change in place (same buffers, new bitstrings)."""
+    import torch
+
+    from paper_2011_02621_b200 import AmplitudeEngine, parse_circuit
+
+    case = golden_amplitudes[0]
+    c = parse_circuit(case["circuit"])
+    outs = [r["out"] for r in case["results"]][:16]
+    eng = AmplitudeEngine(c, case["in_bits"], dtype="complex128")
+    nq = c.num_qubits
+    bits = np.array([[int(ch) for ch in o] for o in outs], dtype=np.int32)
+    sel = eng.selectors(bits)
+    base = eng.amplitudes_device(sel, len(outs)).cpu().numpy()
+    amp = torch.zeros(len(outs), dtype=torch.complex128, device="cuda")
+    for _ in range(3):                     # eager, capture, replay
+        eng.amplitudes_device(sel, len(outs), amp, graph=True)
+    np.testing.assert_allclose(amp.cpu().numpy(), base, atol=1e-13)
+    flipped = 1 - bits
+    sel2 = eng.selectors(flipped)
+    for q in sel:                          # same device buffers, new contents
+        if sel[q] is not None:
+            sel[q].copy_(sel2[q])
+    eng.amplitudes_device(sel, len(outs), amp, graph=True)
+    ref = eng.amplitudes(["".join(map(str, row)) for row in flipped])
+    np.testing.assert_allclose(amp.cpu().numpy(), ref, atol=1e-13)
+    assert nq == bits.shape[1]
