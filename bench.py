@@ -315,7 +315,7 @@ def syc_engine(dev, depth=SYC_DEPTH):
     return AmplitudeEngine(circ, dtype="complex64", max_rank=SYC_MAX_RANK, device=dev)
 
 
-def run_syc53(args, rank, world, dev):
+def run_syc53(args, rank, world, dev, depth=SYC_DEPTH):
     """Amplitudes of the 53-qubit Sycamore circuit (projected engine): each
     step evaluates one batch of B bitstrings (B = the executor's chunk, all
     resident in HBM); each rank evaluates its own bitstrings (weak scaling)."""
@@ -327,7 +327,7 @@ def run_syc53(args, rank, world, dev):
 
     hbm, bf16, peak_src = peaks()
     t0 = time.perf_counter()
-    eng = syc_engine(dev)
+    eng = syc_engine(dev, depth)
     setup_s = time.perf_counter() - t0
     ex, plan = eng.executor, eng.plan
     B = ex.max_z
@@ -387,7 +387,7 @@ def run_syc53(args, rank, world, dev):
                      "path_roofline_frac": tot_roof / tot_t if tot_t else None,
                      "path_roofline": "sum over steps of max(bytes/HBM, flops/bf16 peak) / sum of step times"},
         "config": {"workload": "configs[4] circuit family: 53-qubit Sycamore, ABCDCDAB, "
-                               f"{SYC_DEPTH} cycles (deepest unsliced depth that fits one GPU)",
+                               f"{depth} cycles (unsliced projected network on one GPU)",
                    "dtype": "complex64", "bitstrings_per_step": B, "max_rank": SYC_MAX_RANK,
                    "multiplies_per_amplitude": plan.multiplies, "max_elems": plan.max_elems,
                    "path_steps": len(plan.steps), "host_setup_s": setup_s,
@@ -396,7 +396,8 @@ def run_syc53(args, rank, world, dev):
     }
     if args.e2e:
         outs = ["".join(map(str, row)) for row in bits]
-        eng.amplitudes(outs)
+        for _ in range(2):                       # first call eager, second captures the path's CUDA graph
+            eng.amplitudes(outs)
         torch.cuda.synchronize(dev)
         barrier(world)
         steps = max(1, min(args.steps, 3))
@@ -486,6 +487,8 @@ def run_cfg0(args, rank, world, dev):
     t = allreduce_max(e0.elapsed_time(e1) * 1e-3, world, dev)
     # e2e: host bitstrings in, host amplitudes out, through the public API
     outs = ["".join(map(str, row)) for row in bits]
+    for _ in range(2):                           # eager, then graph capture (untimed)
+        eng.amplitudes(outs)
     t0 = time.perf_counter()
     for _ in range(args.steps):
         eng.amplitudes(outs)
@@ -645,7 +648,7 @@ def main():
     runner = {"sweep": run_sweep, "cfg0": run_cfg0, "syc53": run_syc53}[args.workload]
     res = runner(args, rank, world, dev)
     plan_steps = res.pop("_plan_steps", None)
-    syc = None
+    syc = syc9 = None
     if args.workload == "sweep" and args.syc:
         # the headline circuit family, measured beside the sweep: amplitudes/s of
         # the 53-qubit Sycamore network at the deepest depth one GPU holds
@@ -659,6 +662,22 @@ def main():
                                    "sample": f"numpy tensordot on 2^14-row samples of every distinct step shape, "
                                              f"{spent:.1f}s; scaled by rows (permutation cost not included)"}
         syc["steps"], syc["warmup"] = sargs.steps, sargs.warmup
+        # one cycle deeper: 6.7e12 multiplies and 2^31-element intermediates per
+        # amplitude (one amplitude per device pass), tensor-bound GEMM steps
+        import gc
+
+        gc.collect()
+        torch.cuda.empty_cache()                 # the depth-8 engine's buffers go back first
+        sargs9 = argparse.Namespace(**vars(sargs))
+        sargs9.steps = 3
+        syc9 = run_syc53(sargs9, rank, world, dev, depth=SYC_DEPTH + 1)
+        syc9_steps = syc9.pop("_plan_steps", None)
+        if rank == 0 and args.cpu and world == 1 and syc9_steps:
+            cv, spent = cpu_syc_rate(syc9_steps, min(args.cpu_budget, 10.0))
+            syc9["cpu_baseline"] = {"value": cv, "unit": "amplitudes/s", "cores": _cpu_threads(), "kind": "port",
+                                    "sample": f"numpy tensordot on 2^14-row samples of every distinct step shape, "
+                                              f"{spent:.1f}s; scaled by rows (permutation cost not included)"}
+        syc9["steps"], syc9["warmup"] = sargs9.steps, sargs9.warmup
     if rank == 0:
         if args.cpu and world == 1:
             if args.workload == "sweep":
@@ -677,6 +696,7 @@ def main():
         line = dict(base, **res)
         if syc is not None:
             line["amplitudes_53q"] = syc
+            line["amplitudes_53q_depth9"] = syc9
         print(json.dumps(line))
         if detail is not None:
             (ROOT / "gpurun_out").mkdir(exist_ok=True)

@@ -98,7 +98,10 @@ bool try_skinny(const tnc_step_desc& d, cudaStream_t s) {
   const int64_t N = d.N, K = d.K;
   // few rows (path ends: tiny M, large K or N): one thread per result element
   if (d.Z * d.M < 4096) {
-    tnc::k_step_cols<R><<<grid_for(d.Z * d.M * N, 256), 256, 0, s>>>(d);
+    if (K >= 256 && d.Z * d.M * N <= (int64_t)148 * 64 * 8)   // long K: a warp per result
+      tnc::k_step_dot<R><<<grid_for(d.Z * d.M * N * 32, 256), 256, 0, s>>>(d);
+    else
+      tnc::k_step_cols<R><<<grid_for(d.Z * d.M * N, 256), 256, 0, s>>>(d);
     return true;
   }
   // complex64, K = 2..64 (power of two), N <= 16: warp-cooperative coalesced rows

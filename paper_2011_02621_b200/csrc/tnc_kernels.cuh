@@ -284,6 +284,44 @@ k_step_cols(const __grid_constant__ tnc_step_desc d) {
   }
 }
 
+// Few rows and long K (the last steps of a path: M = 1..256, K = 2^13): one
+// warp per result element, lanes striding over K (coalesced acc row reads),
+// shuffle reduction.
+template <typename R>
+__global__ void __launch_bounds__(256)
+k_step_dot(const __grid_constant__ tnc_step_desc d) {
+  using C = typename cplx<R>::T;
+  const int lane = threadIdx.x & 31;
+  const int64_t total = d.Z * d.M * d.N;
+  const int64_t wstride = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t g = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); g < total; g += wstride) {
+    const int64_t zf = g / d.N, n = g - zf * d.N;
+    const int64_t z = zf / d.M, f = zf - z * d.M;
+    const C* a = reinterpret_cast<const C*>(d.acc) + z * d.acc_zstride + f * d.K;
+    const C* S = reinterpret_cast<const C*>(d.site.ptr) + site_offset(d.site, z, d.slices_per_b, d.s0) + n;
+    C acc = czero<R>();
+    for (int64_t k = lane; k < d.K; k += 32) {
+      C b = __ldg(S + k * d.N);
+      if (d.conj_b) b = cconj(b);
+      cfma(acc, __ldg(a + k), b);
+    }
+    for (int o = 16; o; o >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    if (lane == 0) {
+      C* o = reinterpret_cast<C*>(d.out) + z * d.out_zstride;
+      if (d.c_rows_contig) {
+        o[f * d.N + n] = acc;
+      } else {
+        int64_t oa, oc;
+        row_offsets(d, f, oa, oc);
+        o[oc + d.c_noff[n]] = acc;
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Warp-cooperative skinny step (complex64, K = 2L in {2..64}, N <= NN <= 4):
 // L lanes share one acc row, each loading 16 contiguous bytes (two complex),
