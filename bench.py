@@ -363,12 +363,15 @@ def run_syc53(args, rank, world, dev, depth=SYC_DEPTH):
         NV.check(L.tnc_step(C.byref(ex._steps[i]), sptr), "tnc_step")
         sev[i + 1].record(stream)
     torch.cuda.synchronize(dev)
-    tot_t = tot_roof = gemm_t = gemm_fl = 0.0
+    tot_t = tot_roof = tot_roof3 = gemm_t = gemm_fl = 0.0
     for i, sp in enumerate(plan.steps):
         ts = sev[i].elapsed_time(sev[i + 1]) * 1e-3
         by, fl = traffic[i][0] * B, traffic[i][1] * B
         tot_t += ts
         tot_roof += max(by / (hbm * 1e9), fl / (bf16 * 1e12))
+        # the fp16-split GEMM issues 3 products per real product: its own tensor ceiling is bf16/3
+        split = sp.K * sp.N >= 256 and sp.K % 16 == 0
+        tot_roof3 += max(by / (hbm * 1e9), (3 * fl if split else fl) / (bf16 * 1e12))
         if sp.K * sp.N >= 256 and sp.K % 8 == 0:      # tensor-core steps
             gemm_t += ts
             gemm_fl += fl
@@ -385,7 +388,10 @@ def run_syc53(args, rank, world, dev, depth=SYC_DEPTH):
                      "algorithmic": "8*M*K*N flops per step per bitstring",
                      "kernel_share_of_step": gemm_t / tot_t if tot_t else None,
                      "path_roofline_frac": tot_roof / tot_t if tot_t else None,
-                     "path_roofline": "sum over steps of max(bytes/HBM, flops/bf16 peak) / sum of step times"},
+                     "path_roofline": "sum over steps of max(bytes/HBM, flops/bf16 peak) / sum of step times",
+                     "path_roofline_frac_split": tot_roof3 / tot_t if tot_t else None,
+                     "path_roofline_split": "same with 3x flops on the fp16-split GEMM steps (the complex64 "
+                                            "accuracy bound needs 3 fp16 products per real product)"},
         "config": {"workload": "configs[4] circuit family: 53-qubit Sycamore, ABCDCDAB, "
                                f"{depth} cycles (unsliced projected network on one GPU)",
                    "dtype": "complex64", "bitstrings_per_step": B, "max_rank": SYC_MAX_RANK,
