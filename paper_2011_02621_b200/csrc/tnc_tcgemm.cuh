@@ -52,6 +52,7 @@ struct GemmDesc {
   const unsigned char* bp;       // [combo][tile_n][chunk][hi: -Bi|Br|Bi][lo: -Bi|Br|Bi][NT x KC] canonical
   int64_t bp_combo_stride;       // bytes per combo
   int32_t f16, cn_smem;          // 1: fp16 split operands (needs amax_in); c_noff staged in smem (int32)
+  int32_t blk_contig, _pad6;     // 1: every warp's 32 rows x 16 columns block is one contiguous 4 KB run
   const float* amax_in;          // [Z] max |re|,|im| of acc[z] (F16 scale)
   float* amax_out;               // [Z] max |re|,|im| of out[z] (zeroed by the host), or null
   const float* bscale;           // [combo] max |re|,|im| of the site block (F16)
@@ -430,7 +431,7 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
     // staged n-major stores when the innermost result leg is a new leg (runs
     // of consecutive n are contiguous); per-row stores otherwise (then the
     // innermost result leg is a free leg: consecutive rows are contiguous)
-    const bool staged = p.c_rows_contig || p.n_contig || (p.N > 1 && p.c_noff[1] == p.c_noff[0] + 1);
+    const bool staged = !(p.dbg & 8) && (p.c_rows_contig || p.n_contig || (p.N > 1 && p.c_noff[1] == p.c_noff[0] + 1));
     const int cfirst = alt ? 0 : eg * 16, cstep = alt ? 16 : 16 * EPIG;
     float inv = 1.f, inv2 = 1.f;
     int64_t inv_z = -1;
@@ -560,6 +561,22 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
                          "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
           }
           __syncwarp();
+          if (p.blk_contig && ncols == 16 && mt * 128 + q * 32 + 32 <= p.M) {
+            // the warp's 32 rows x 16 columns are one contiguous 4 KB run:
+            // eight fully coalesced 512-byte stores, no per-row addressing
+            const int64_t oc0 = __shfl_sync(0xffffffffu, oc, 0);
+            float4* dst = reinterpret_cast<float4*>(O + oc0 + (p.c_rows_contig ? n0 + c0 : (int64_t)cn_s[n0 + c0]));
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int c = i * 32 + lane;
+              float4 v;
+              asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                           : "r"(stg_s + (c >> 3) * TG_EPI_PITCH + (c & 7) * 16) : "memory");
+              dst[c] = v;
+            }
+            __syncwarp();
+            continue;
+          }
           const int sub = lane & 7;                // 16-byte piece (2 complex) of a row
           const int64_t n = n0 + c0 + 2 * sub;
           int64_t a0 = 0, a1 = 0;
@@ -931,6 +948,14 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
     int RS = 4, BS = 3;
     const size_t budget = 226 * 1024;
     p.cn_smem = (!d.c_rows_contig && d.N <= 1024 && d.out_zstride < 0x7fffffffLL) ? 1 : 0;
+    // contiguous 32 x 16 blocks: innermost free leg (>= 32 rows) at stride 16 and
+    // 16 consecutive columns contiguous (innermost new leg of extent % 16 == 0 at stride 1)
+    p.blk_contig = 0;
+    if (d.nf >= 1 && d.f_dim[d.nf - 1] % 32 == 0 && d.f_cstride[d.nf - 1] == 16 && d.M % 128 == 0) {
+      if (d.c_rows_contig && d.N == 16) p.blk_contig = 1;
+      else if (!d.c_rows_contig && p.cn_smem && d.nn > 0 && d.n_dim[d.nn - 1] % 16 == 0 && d.n_cstride[d.nn - 1] == 1)
+        p.blk_contig = 1;
+    }
     const int64_t cn = p.cn_smem ? d.N : 0;
     CUtensorMap tmO;
     const int tma = tg_out_map(d, p, tmO, enc) ? 1 : 0;
