@@ -53,6 +53,7 @@ struct GemmDesc {
   int64_t bp_combo_stride;       // bytes per combo
   int32_t f16, cn_smem;          // 1: fp16 split operands (needs amax_in); c_noff staged in smem (int32)
   int32_t blk_contig, _pad6;     // 1: every warp's 32 rows x 16 columns block is one contiguous 4 KB run
+  int64_t row_stride;            // != 0: rows r..r+31 of a warp block sit at oc(r) + i * row_stride
   const float* amax_in;          // [Z] max |re|,|im| of acc[z] (F16 scale)
   float* amax_out;               // [Z] max |re|,|im| of out[z] (zeroed by the host), or null
   const float* bscale;           // [combo] max |re|,|im| of the site block (F16)
@@ -582,11 +583,13 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
           int64_t a0 = 0, a1 = 0;
           if (2 * sub < ncols) a0 = p.c_rows_contig ? n : (p.cn_smem ? cn_s[n] : p.c_noff[n]);
           if (2 * sub + 1 < ncols) a1 = p.c_rows_contig ? n + 1 : (p.cn_smem ? cn_s[n + 1] : p.c_noff[n + 1]);
+          // rows of a warp at one stride (innermost free leg >= 32 rows): no shuffles
+          const int64_t oc0 = p.row_stride ? __shfl_sync(0xffffffffu, oc, 0) : 0;
 #pragma unroll
           for (int rr = 0; rr < 32; rr += 4) {
             const int lr = rr + (lane >> 3);
             const int64_t grow = mt * 128 + q * 32 + lr;
-            const int64_t ocr = __shfl_sync(0xffffffffu, oc, lr);
+            const int64_t ocr = p.row_stride ? oc0 + (int64_t)lr * p.row_stride : __shfl_sync(0xffffffffu, oc, lr);
             if (grow < p.M && 2 * sub < ncols) {
               float4 v;
               asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
@@ -951,6 +954,8 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
     // contiguous 32 x 16 blocks: innermost free leg (>= 32 rows) at stride 16 and
     // 16 consecutive columns contiguous (innermost new leg of extent % 16 == 0 at stride 1)
     p.blk_contig = 0;
+    p.row_stride = (d.c_rows_contig && d.M % 32 == 0) ? d.N
+                   : ((d.nf >= 1 && d.f_dim[d.nf - 1] % 32 == 0) ? d.f_cstride[d.nf - 1] : 0);
     if (d.nf >= 1 && d.f_dim[d.nf - 1] % 32 == 0 && d.f_cstride[d.nf - 1] == 16 && d.M % 128 == 0) {
       if (d.c_rows_contig && d.N == 16) p.blk_contig = 1;
       else if (!d.c_rows_contig && p.cn_smem && d.nn > 0 && d.n_dim[d.nn - 1] % 16 == 0 && d.n_cstride[d.nn - 1] == 1)
