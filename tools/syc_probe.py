@@ -27,7 +27,8 @@ def main():
     graph, pats, _ = sycamore53_graph()
     circ = pattern_rqc(graph, [pats[c] for c in "ABCDCDAB"], depth, seed=0)
     t0 = time.perf_counter()
-    eng = AmplitudeEngine(circ, dtype="complex64", max_rank=12)
+    dtype = "complex128" if "--c128" in sys.argv else "complex64"
+    eng = AmplitudeEngine(circ, dtype=dtype, max_rank=12)
     t_setup = time.perf_counter() - t0
     plan, ex = eng.plan, eng.executor
     print(f"depth {depth}: setup {t_setup:.1f}s steps {len(plan.steps)} max_elems 2^{np.log2(plan.max_elems):.1f} "
@@ -35,7 +36,7 @@ def main():
     rng = np.random.default_rng(0)
     bits = rng.integers(0, 2, (B, 53)).astype(np.int32)
     sel = eng.selectors(bits)
-    amp = torch.zeros(B, dtype=torch.complex64, device="cuda")
+    amp = torch.zeros(B, dtype=getattr(torch, dtype), device="cuda")
     for _ in range(2):
         eng.amplitudes_device(sel, B, amp)
     torch.cuda.synchronize()
@@ -71,7 +72,7 @@ def main():
     z = nb * ns
     ex.run(sel, nb, amp)        # binds descriptors for this chunk
     pd = ex._pd
-    traffic = plan.step_traffic(8)
+    traffic = plan.step_traffic(16 if dtype == "complex128" else 8)
     rows = []
     passes = int(sys.argv[sys.argv.index("--passes") + 1]) if "--passes" in sys.argv else 3
     best = [float("inf")] * len(plan.steps)
