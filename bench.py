@@ -25,7 +25,8 @@ Workloads (``--workload``):
 
 Timing: W warm-up steps, then K steps; every case (a timed iteration) is
 bracketed by CUDA events on the launching stream and preceded by an untimed
-L2 flush (256 MiB memset), so no case reads L2-resident data; barrier +
+L2 flush (256 MiB memset, then a 256 MiB read so the flush's dirty lines are
+written back before the timed kernel), so no case reads L2-resident data; barrier +
 synchronize around the timed region; max over ranks.  ``--impl reference``
 times the CPU oracle port of the reference algorithm (numpy tensordot, as
 tnsim.tensor.contract_pair) on a bounded sample and scales to the same unit.
@@ -165,6 +166,9 @@ def run_sweep(args, rank, world, dev):
     acc = torch.randn(max_acc, dtype=torch.complex64, device=dev)
     out = torch.empty(max_out, dtype=torch.complex64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush_f = flush.view(torch.float32)
+    flush_sink = torch.empty((), dtype=torch.float32, device=dev)
+    l2_mode = os.environ.get("BENCH_L2_FLUSH", "write+read")
     plans, inputs = [], []
     gen = torch.Generator(device=dev)
     gen.manual_seed(99 + rank)
@@ -184,7 +188,12 @@ def run_sweep(args, rank, world, dev):
         for ci, (r, k, n, B) in enumerate(cases):
             variants, bits, site = inputs[ci]
             KN = 4 ** (k + n)
+            # untimed L2 flush: write a buffer larger than L2, then read it back,
+            # so the flush's own dirty lines are written back before the timed
+            # kernel instead of during it
             flush.zero_()
+            if l2_mode == "write+read":
+                torch.sum(flush_f, dim=0, out=flush_sink)
             e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
             e0.record(stream)
             project_variants(variants, bits, site, KN, stream)
@@ -246,7 +255,8 @@ def run_sweep(args, rank, world, dev):
                    "cases": len(cases), "r": [16, 20, 24, 28], "k": [1, 2, 3], "n": [1, 2, 3],
                    "batch": [1, 16, 256], "operand_limit_elems": args.limit,
                    "leg_order": "seeded random permutation per case",
-                   "l2": "256 MiB memset flush before every case (untimed)"},
+                   "l2": ("256 MiB memset + 256 MiB read (write-back of the flush drained) before every case, untimed"
+                          if l2_mode == "write+read" else "256 MiB memset flush before every case (untimed)")},
         "clocks": clk.summary(),
         "dtype": "complex64",
         "detail": detail,
