@@ -500,26 +500,31 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
     const int q = warp & 3;                      // lane quarter
     const int r = q * 32 + lane;                 // tile row
     unsigned char* stg = epi_stage + (eg * 4 + q) * 32 * TC_EPI_PITCH;
+    // tile -> (z, row block) tracked incrementally (this group steps by 2 tiles)
+    int64_t zt = (g0 + eg) / p.tiles_per_z, mb = (g0 + eg) - zt * p.tiles_per_z;
+    int64_t inv2_z = -1;
+    float inv2 = 1.f;
     for (int t = eg; t < ntiles; t += 2) {
       const int acc = t % TS;
       const uint32_t ph = (t / TS) & 1;
+      if (t != eg) {
+        mb += 2;
+        while (mb >= p.tiles_per_z) { mb -= p.tiles_per_z; ++zt; }
+      }
       if (q == 0) TC_TRACE(3, t);
       mbar_wait_spin(&tfull[acc], ph);
       if (q == 0) TC_TRACE(4, t);
       tc_fence_after();
-      const int64_t gt = g0 + t;
-      const int64_t zt = gt / p.tiles_per_z;
-      const int64_t grow = (gt - zt * p.tiles_per_z) * 128 + r;
+      const int64_t grow = mb * 128 + r;
       float2* otile = p.out + zt * p.out_zstride + (grow - lane) * N;   // this warp's 32 rows
       const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * Nr);
-      float inv = 1.f, inv2 = 1.f;
+      float inv = 1.f;
+      uint32_t iv = 0;
       if constexpr (F16) {
-        inv2 = 1.f / tc_f16_scale(__ldg(p.bscale + zt));
-        uint32_t iv;
+        if (zt != inv2_z) { inv2_z = zt; inv2 = 1.f / tc_f16_scale(__ldg(p.bscale + zt)); }
+        // the row's inverse scale rides along with the first accumulator read (one wait)
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
                      : "=r"(iv) : "r"(tmem + ((uint32_t)(q * 32) << 16) + SCOL + (uint32_t)acc));
-        tmem_wait_ld();
-        inv = __uint_as_float(iv);
       }
       for (int c0 = 0; c0 < Nr; c0 += 32) {
         const int cols = (c0 + 32 <= Nr) ? 32 : 16;
@@ -536,6 +541,7 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
           for (int j = 0; j < 16; ++j) v[j] = w16[j];
         }
         tmem_wait_ld();
+        if constexpr (F16) inv = __uint_as_float(iv);
         if (q == 0 && c0 == 0) TC_TRACE(14, t);
         if (c0 + 32 >= Nr) {              // accumulator drained: hand it back before the stores
           tc_fence_before();
@@ -554,11 +560,14 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
         if (q == 0 && c0 == 0) TC_TRACE(15, t);
         const int real = min(cols, 2 * N - c0);        // real (unpadded) columns in this chunk
         const int per_row = real / 4;
+        // per_row is 2, 4 or 8 for the padded widths: shifts instead of divisions
+        const int prs = (per_row & (per_row - 1)) == 0 ? __ffs(per_row) - 1 : -1;
         if (!(p.dbg & 1) && per_row > 0) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int idx = i * 32 + lane;
-            const int row = idx / per_row, piece = idx - row * per_row;
+            const int row = prs >= 0 ? idx >> prs : idx / per_row;
+            const int piece = idx - row * per_row;
             if (row < 32) {
               const uint4 val = *reinterpret_cast<const uint4*>(stg + row * TC_EPI_PITCH + piece * 16);
               *reinterpret_cast<uint4*>(reinterpret_cast<unsigned char*>(otile + (int64_t)row * N + c0 / 2) + piece * 16) = val;
@@ -735,10 +744,11 @@ __host__ inline int launch_tc(TcDesc p, int64_t Z, cudaStream_t s) {
   // ring holds whole tiles and the chunks are 16 complex (kind::f16 K = 16)
   int TS16, AS16;
   tc_tmem_plan(p.K, tc_npad(p.N), TS16, AS16, true);
-  const char* e16 = getenv("TNC_TC16");
-  // (K = 16 only: with several chunks per tile the per-row scale needs an extra
-  // pass over the staged tile, which measured slower than 3xTF32 at K = 64)
-  p.f16 = (kc == 16 && p.K == 16 && p.raw_stages > 0 && AS16 >= 2 && !(e16 && e16[0] == '0')) ? 1 : 0;
+  // opt-in (TNC_TC_F16=1, K = 16 only): measured 7% faster on some K=N=16 leg
+  // orders but up to 3.7x slower on others (the per-row max pass over the
+  // staged tile; converters held back by the accumulator stages when N >= 64)
+  const char* e16 = getenv("TNC_TC_F16");
+  p.f16 = (kc == 16 && p.K == 16 && p.raw_stages > 0 && AS16 >= 2 && e16 && e16[0] == '1') ? 1 : 0;
   float* bsc = nullptr;
   if (p.f16) {
     if (cudaMallocAsync(reinterpret_cast<void**>(&bsc), (size_t)Z * sizeof(float), s) != cudaSuccess) return -1;
