@@ -105,6 +105,21 @@ __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t phase) {
       "bra WAIT_%=;\n\t"
       "DONE_%=:\n\t}" ::"r"(smem_u32(bar)), "r"(phase) : "memory");
 }
+// Keep freed stream-ordered blocks in the device's default pool across
+// synchronizations (the default release threshold returns them to the OS at
+// every sync, and the next cudaMallocAsync would map memory again: ~1 ms).
+inline void pool_keep() {
+  static int pool_dev = -1;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (pool_dev == cur) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, cur) == cudaSuccess) {
+    uint64_t thr = 1ull << 30;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  pool_dev = cur;
+}
 // generic-proxy shared-memory accesses of this thread ordered against the async proxy (TMA / bulk copies / tcgen05)
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 // global -> shared bulk copy completing on `bar` (16-byte aligned, size % 16 == 0)

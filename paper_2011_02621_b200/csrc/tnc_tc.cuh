@@ -152,15 +152,16 @@ __host__ __device__ inline int64_t tc_smem_bytes(int64_t K, int64_t N, int64_t p
          + TC_EPI_WARPS * 32 * TC_EPI_PITCH + 16 + rs * tc_raw_bytes(K);
 }
 // TMEM plan: TS accumulators of Nr columns, AS A-chunk stages of 4*KC columns (hi + lo)
-// f16: A stages of 2*kc columns (two fp16 per column) and TS columns at the
-// top of TMEM for the per-row inverse scales of each accumulator stage
+// f16: A stages of 2*kc columns (two fp16 per column) and TC_SCALE_COLS
+// columns at the top of TMEM: a ring of per-row inverse scales indexed by tile
+constexpr int TC_SCALE_COLS = 32;
 __host__ __device__ inline void tc_tmem_plan(int64_t K, int64_t N, int& TS, int& AS, bool f16 = false) {
   const int Nr = (int)(2 * N), kc = (int)tc_kc(K);
   TS = 256 / Nr;
   if (TS > TC_MAX_STAGES) TS = TC_MAX_STAGES;
   TS &= ~1;                                     // even: each epilogue group owns its stages
   if (TS < 2) TS = 2;
-  AS = f16 ? (512 - TS * Nr - TS) / (2 * kc) : (512 - TS * Nr) / (4 * kc);
+  AS = f16 ? (512 - TS * Nr - TC_SCALE_COLS) / (2 * kc) : (512 - TS * Nr) / (4 * kc);
   if (AS > TC_MAX_STAGES) AS = TC_MAX_STAGES;
 }
 
@@ -319,7 +320,11 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
   const uint32_t A0 = (uint32_t)(TS * Nr);      // first A column
   // per A stage: tf32 hi (2KC) + lo (2KC) columns; f16 hi (KC) + lo (KC), one complex per column
   constexpr uint32_t ACOLS = F16 ? 2 * KC : 4 * KC;
-  const uint32_t SCOL = 512u - (uint32_t)TS;    // f16: column SCOL + acc = per-row inverse scales
+  // f16: column SCOL + t % TC_SCALE_COLS holds tile t's per-row inverse scales.  A
+  // converter is at most AS + TS tiles ahead of the epilogue's scale read
+  // (A stages, then accumulator stages), and AS + TS <= 16 < TC_SCALE_COLS,
+  // so a column is never rewritten before it has been read -- no extra wait
+  const uint32_t SCOL = 512u - (uint32_t)TC_SCALE_COLS;
   // ---- shared memory carve-up ----
   float* Bhi = reinterpret_cast<float*>(smem_raw);
   float* Blo = Bhi + (size_t)Nr * Kr;
@@ -424,22 +429,19 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
       }
       const float2* Ar = A + tbase[t];
       float sA = 1.f;
+      bool scale_pending = false;
       if constexpr (F16) {
-        // per-row scale from the whole row (the raw stage holds the full 128 x K tile)
-        float m = 0.f;
-        for (int k = 0; k < K; ++k) {
-          const float2 x = raw[kraw_s[k]];
-          m = fmaxf(m, fmaxf(fabsf(x.x), fabsf(x.y)));
+        if (nchunk > 1) {
+          // per-row scale from the whole row (the raw stage holds the full 128 x K tile)
+          float m = 0.f;
+          for (int k = 0; k < K; ++k) {
+            const float2 x = raw[kraw_s[k]];
+            m = fmaxf(m, fmaxf(fabsf(x.x), fabsf(x.y)));
+          }
+          sA = tc_f16_scale(m);
+        } else {
+          scale_pending = true;                  // one chunk: the row max comes from its registers below
         }
-        sA = tc_f16_scale(m);
-        const float inv = 1.f / sA;              // the site factor 1/t(z) is applied by the epilogue
-        // the accumulator stage's scale column is free once its previous tile is drained
-        const int acc = t % TS;
-        mbar_wait_spin(&tempty[acc], (uint32_t)(((t / TS) & 1) ^ 1));
-        tc_fence_after();
-        uint32_t iv[1] = {__float_as_uint(inv)};
-        asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};"
-                     ::"r"(tmem + lane_base + SCOL + (uint32_t)acc), "r"(iv[0]));
       }
       for (int c = 0; c < nchunk; ++c, ++j) {
         const int stage = grp * ASg + j % ASg;
@@ -454,10 +456,24 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
 #pragma unroll
           for (int q = 0; q < KC; ++q) v[q] = (p.dbg & 2) ? make_float2(1.f, 0.f) : __ldg(Ar + ko[q]);
         }
+        if constexpr (F16) {
+          if (scale_pending) {
+            float m = 0.f;
+#pragma unroll
+            for (int q = 0; q < KC; ++q) m = fmaxf(m, fmaxf(fabsf(v[q].x), fabsf(v[q].y)));
+            sA = tc_f16_scale(m);
+            scale_pending = false;
+          }
+        }
         mbar_wait_spin(&empty[stage], ph ^ 1);
         tc_fence_after();
         const uint32_t col = A0 + (uint32_t)stage * ACOLS;
         if constexpr (F16) {
+          if (c == 0) {                          // tile's inverse row scales (site factor 1/t(z) in the epilogue)
+            const uint32_t iv = __float_as_uint(1.f / sA);
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};"
+                         ::"r"(tmem + lane_base + SCOL + (uint32_t)(t % TC_SCALE_COLS)), "r"(iv));
+          }
           uint32_t hi[KC], lo[KC];
 #pragma unroll
           for (int q = 0; q < KC; ++q) tc_split_f16x2(v[q].x * sA, v[q].y * sA, hi[q], lo[q]);
@@ -524,7 +540,7 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
         if (zt != inv2_z) { inv2_z = zt; inv2 = 1.f / tc_f16_scale(__ldg(p.bscale + zt)); }
         // the row's inverse scale rides along with the first accumulator read (one wait)
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
-                     : "=r"(iv) : "r"(tmem + ((uint32_t)(q * 32) << 16) + SCOL + (uint32_t)acc));
+                     : "=r"(iv) : "r"(tmem + ((uint32_t)(q * 32) << 16) + SCOL + (uint32_t)(t % TC_SCALE_COLS)));
       }
       for (int c0 = 0; c0 < Nr; c0 += 32) {
         const int cols = (c0 + 32 <= Nr) ? 32 : 16;
@@ -744,13 +760,14 @@ __host__ inline int launch_tc(TcDesc p, int64_t Z, cudaStream_t s) {
   // ring holds whole tiles and the chunks are 16 complex (kind::f16 K = 16)
   int TS16, AS16;
   tc_tmem_plan(p.K, tc_npad(p.N), TS16, AS16, true);
-  // opt-in (TNC_TC_F16=1, K = 16 only): measured 7% faster on some K=N=16 leg
-  // orders but up to 3.7x slower on others (the per-row max pass over the
-  // staged tile; converters held back by the accumulator stages when N >= 64)
+  // (K = 16 only: one chunk per tile, so the row max comes from the values
+  // being converted; at K = 64 the extra pass over the staged tile measured
+  // slower than 3xTF32.  TNC_TC_F16=0 forces 3xTF32.)
   const char* e16 = getenv("TNC_TC_F16");
-  p.f16 = (kc == 16 && p.K == 16 && p.raw_stages > 0 && AS16 >= 2 && e16 && e16[0] == '1') ? 1 : 0;
+  p.f16 = (kc == 16 && p.K == 16 && p.raw_stages > 0 && AS16 >= 2 && !(e16 && e16[0] == '0')) ? 1 : 0;
   float* bsc = nullptr;
   if (p.f16) {
+    pool_keep();
     if (cudaMallocAsync(reinterpret_cast<void**>(&bsc), (size_t)Z * sizeof(float), s) != cudaSuccess) return -1;
     p.bscale = bsc;
     k_tc_bmax<<<(unsigned)std::min<int64_t>(Z, 4096), 128, 0, s>>>(p, bsc);

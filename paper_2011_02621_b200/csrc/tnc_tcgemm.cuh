@@ -982,22 +982,7 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
       return 0;
     p.bp_combo_stride = (int64_t)p.tiles_n * p.nchunk * 6 * tg_block_bytes(p.NT, KC, f16);
     unsigned char* bp = nullptr;
-    {
-      // keep freed stream-ordered blocks in the device pool across synchronizations
-      // (the default threshold returns them to the OS at every sync, and the next
-      // step's allocation would re-map memory)
-      static int pool_dev = -1;
-      int cur = 0;
-      cudaGetDevice(&cur);
-      if (pool_dev != cur) {
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, cur) == cudaSuccess) {
-          uint64_t thr = 1ull << 30;
-          cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
-        pool_dev = cur;
-      }
-    }
+    pool_keep();
     // one allocation: B' blocks, then (F16) the per-combo site maxima
     const size_t bp_bytes = ((size_t)combos * p.bp_combo_stride + 255) & ~(size_t)255;
     if (cudaMallocAsync(reinterpret_cast<void**>(&bp), bp_bytes + (f16 ? combos * 4 : 0), s) != cudaSuccess) return -1;
