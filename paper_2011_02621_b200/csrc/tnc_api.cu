@@ -33,6 +33,15 @@ int tc_mask() {
   return v;
 }
 bool tc_enabled() { return tc_mask() != 0; }
+// pairwise plans: smallest K*N routed to the tensor-core kernel (TNC_TC_MIN_KN)
+int64_t tc_min_kn() {
+  static int64_t v = -1;
+  if (v < 0) {
+    const char* e = getenv("TNC_TC_MIN_KN");
+    v = e ? atoll(e) : 256;
+  }
+  return v;
+}
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -719,7 +728,7 @@ void bind_tables(tnc_pair_plan& P, void* dev) {
 int execute_pair_plan(const tnc_pair_plan& P, int64_t batch, const void* a, int64_t a_zstride, const void* b,
                       int64_t b_zstride, void* out, int64_t out_zstride, cudaStream_t s) {
   if (batch <= 0) return TNC_OK;
-  if (P.tc_ok && (tc_mask() & 1) && P.tc.K * P.tc.N >= 256) {
+  if (P.tc_ok && (tc_mask() & 1) && P.tc.K * P.tc.N >= tc_min_kn()) {
     tnc::TcDesc c = P.tc;
     c.a = reinterpret_cast<const float2*>(a);
     c.a_zstride = a_zstride;
@@ -812,7 +821,7 @@ int tnc_pair_plan_execute(const tnc_pair_plan* plan, int64_t batch, const void* 
 
 int tnc_pair_plan_kernel(const tnc_pair_plan* plan) {
   if (!plan) return TNC_E_INVALID;
-  if (plan->tc_ok && (tc_mask() & 1) && plan->tc.K * plan->tc.N >= 256) return TNC_K_TC;
+  if (plan->tc_ok && (tc_mask() & 1) && plan->tc.K * plan->tc.N >= tc_min_kn()) return TNC_K_TC;
   return plan->kind;
 }
 
