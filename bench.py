@@ -327,8 +327,11 @@ def syc_engine(dev, depth=SYC_DEPTH):
 
 def run_syc53(args, rank, world, dev, depth=SYC_DEPTH):
     """Amplitudes of the 53-qubit Sycamore circuit (projected engine): each
-    step evaluates one batch of B bitstrings (B = the executor's chunk, all
-    resident in HBM); each rank evaluates its own bitstrings (weak scaling)."""
+    step evaluates one batch of B bitstrings per GPU (B = the executor's chunk,
+    all resident in HBM).  With N ranks the step is one global batch of N*B
+    bitstrings through ``distributed.sharded_amplitudes``: every rank contracts
+    its shard, one NCCL all-reduce sums and gathers the amplitudes (weak
+    scaling: B per rank)."""
     import ctypes as C
 
     import torch
@@ -341,13 +344,26 @@ def run_syc53(args, rank, world, dev, depth=SYC_DEPTH):
     setup_s = time.perf_counter() - t0
     ex, plan = eng.executor, eng.plan
     B = ex.max_z
-    rng = np.random.default_rng(100 + rank)
-    bits = rng.integers(0, 2, (B, 53)).astype(np.int32)
+    from paper_2011_02621_b200.distributed import sharded_amplitudes
+
+    Bg = B * world                              # the global batch (same bitstrings on every rank)
+    rng = np.random.default_rng(100)
+    gbits = rng.integers(0, 2, (Bg, 53)).astype(np.int32)
+    gsel = eng.selectors(gbits)
+    gamp = torch.zeros(Bg, dtype=torch.complex64, device=dev)
+
+    def one_pass():
+        if world > 1:
+            sharded_amplitudes(ex, gsel, Bg, gamp)
+        else:
+            eng.amplitudes_device(gsel, B, gamp)
+
+    bits = gbits[rank * B:(rank + 1) * B]
     sel = eng.selectors(bits)
     amp = torch.zeros(B, dtype=torch.complex64, device=dev)
     stream = torch.cuda.current_stream(dev)
     for _ in range(args.warmup):
-        eng.amplitudes_device(sel, B, amp)
+        one_pass()
     barrier(world)
     torch.cuda.synchronize(dev)
     # each step's working set (2 x B x 4 GiB ping-pong buffers) is far larger than L2
@@ -355,7 +371,7 @@ def run_syc53(args, rank, world, dev, depth=SYC_DEPTH):
     with ClockSampler(dev.index) as clk:
         for e0, e1 in evs:
             e0.record(stream)
-            eng.amplitudes_device(sel, B, amp)
+            one_pass()
             e1.record(stream)
         torch.cuda.synchronize(dev)
     t = sum(e0.elapsed_time(e1) for e0, e1 in evs) * 1e-3
@@ -405,6 +421,9 @@ def run_syc53(args, rank, world, dev, depth=SYC_DEPTH):
         "config": {"workload": "configs[4] circuit family: 53-qubit Sycamore, ABCDCDAB, "
                                f"{depth} cycles (unsliced projected network on one GPU)",
                    "dtype": "complex64", "bitstrings_per_step": B, "max_rank": SYC_MAX_RANK,
+                   "sharding": ("one global batch of N*B bitstrings: per-rank shard (distributed.rank_chunks) + "
+                                "one NCCL all_reduce(sum) of the amplitude vector, timed" if world > 1
+                                else "single GPU"),
                    "multiplies_per_amplitude": plan.multiplies, "max_elems": plan.max_elems,
                    "path_steps": len(plan.steps), "host_setup_s": setup_s,
                    "l2": "inputs larger than L2 (2 x B x 4 GiB ping-pong buffers)"},

@@ -765,6 +765,10 @@ __host__ inline int launch_tc(TcDesc p, int64_t Z, cudaStream_t s) {
   // slower than 3xTF32.  TNC_TC_F16=0 forces 3xTF32.)
   const char* e16 = getenv("TNC_TC_F16");
   p.f16 = (kc == 16 && p.K == 16 && p.raw_stages > 0 && AS16 >= 2 && !(e16 && e16[0] == '0')) ? 1 : 0;
+  if (getenv("TNC_TC_VERBOSE"))
+    fprintf(stderr, "launch_tc K=%lld N=%lld M=%lld Z=%lld f16=%d raw_stages=%d AS16=%d per=%lld grid=%lld Kout=%lld Lseg=%lld\n",
+            (long long)p.K, (long long)p.N, (long long)p.M, (long long)Z, p.f16, p.raw_stages, AS16,
+            (long long)per, (long long)grid, (long long)p.Kout, (long long)p.Lseg);
   float* bsc = nullptr;
   if (p.f16) {
     pool_keep();
