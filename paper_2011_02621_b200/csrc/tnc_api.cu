@@ -42,6 +42,9 @@ int64_t tc_min_kn() {
   }
   return v;
 }
+// measured: K <= 4 stays on the SIMT column kernel (16-byte stores, 3.8 vs
+// 3.5 TB/s at K=4, N=64); K >= 8 with K*N >= 256 goes to tcgen05
+bool pair_use_tc(int64_t K, int64_t N) { return K * N >= tc_min_kn() && K >= 8; }
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -276,7 +279,14 @@ int launch_pair_tiled(const tnc::PairTile& p, int64_t batch, const void* a, cons
   using C = typename tnc::cplx<R>::T;
   const int64_t N = p.N, K = p.K;
   if (p.pipe && pipe_eligible(p, sizeof(C), a)) {
-    if (N >= 8 && N <= 256 && (256 % N) == 0 && K <= (sizeof(R) == 4 ? 64 : 16)) {
+    static const bool cols_ok = !(getenv("TNC_PIPE_COLS") && getenv("TNC_PIPE_COLS")[0] == '0');
+    if (cols_ok && N >= 8 && N <= 256 && (256 % N) == 0 && K <= (sizeof(R) == 4 ? 64 : 16)) {
+      // two columns per thread (16-byte stores) when the rows stay 16-byte aligned
+      static const bool nv2 = !(getenv("TNC_PIPE_NV2") && getenv("TNC_PIPE_NV2")[0] == '0');
+      if (nv2 && sizeof(R) == 4 && N >= 16 && ((uintptr_t)out % 16) == 0) {
+        if (K <= 4) return launch_pipe_fn<R>(tnc::k_pair_pipe_cols<R, 4, 2>, p, batch, a, b, out, s, true);
+        if (K <= 16) return launch_pipe_fn<R>(tnc::k_pair_pipe_cols<R, 16, 2>, p, batch, a, b, out, s, true);
+      }
       if (K <= 4) return launch_pipe_fn<R>(tnc::k_pair_pipe_cols<R, 4>, p, batch, a, b, out, s, true);
       if (K <= 16) return launch_pipe_fn<R>(tnc::k_pair_pipe_cols<R, 16>, p, batch, a, b, out, s, true);
       if constexpr (sizeof(R) == 4) return launch_pipe_fn<R>(tnc::k_pair_pipe_cols<R, 64>, p, batch, a, b, out, s, true);
@@ -728,7 +738,7 @@ void bind_tables(tnc_pair_plan& P, void* dev) {
 int execute_pair_plan(const tnc_pair_plan& P, int64_t batch, const void* a, int64_t a_zstride, const void* b,
                       int64_t b_zstride, void* out, int64_t out_zstride, cudaStream_t s) {
   if (batch <= 0) return TNC_OK;
-  if (P.tc_ok && (tc_mask() & 1) && P.tc.K * P.tc.N >= tc_min_kn()) {
+  if (P.tc_ok && (tc_mask() & 1) && pair_use_tc(P.tc.K, P.tc.N)) {
     tnc::TcDesc c = P.tc;
     c.a = reinterpret_cast<const float2*>(a);
     c.a_zstride = a_zstride;
@@ -821,7 +831,7 @@ int tnc_pair_plan_execute(const tnc_pair_plan* plan, int64_t batch, const void* 
 
 int tnc_pair_plan_kernel(const tnc_pair_plan* plan) {
   if (!plan) return TNC_E_INVALID;
-  if (plan->tc_ok && (tc_mask() & 1) && plan->tc.K * plan->tc.N >= tc_min_kn()) return TNC_K_TC;
+  if (plan->tc_ok && (tc_mask() & 1) && pair_use_tc(plan->tc.K, plan->tc.N)) return TNC_K_TC;
   return plan->kind;
 }
 

@@ -312,7 +312,7 @@ namespace tnc {
 // column S[:, n] lives in registers, and the accumulator values a[row][k] are
 // warp broadcasts (N >= 32) or few-way reads from the staged tile.
 // ---------------------------------------------------------------------------
-template <typename R, int KMAX>
+template <typename R, int KMAX, int NV = 1>
 __global__ void __launch_bounds__(256, 1)
 k_pair_pipe_cols(const __grid_constant__ PairTile p, const void* __restrict__ A_, const void* __restrict__ B_,
                  void* __restrict__ O_, int64_t tiles_total, int64_t tiles_per_cta) {
@@ -340,10 +340,13 @@ k_pair_pipe_cols(const __grid_constant__ PairTile p, const void* __restrict__ A_
   __syncthreads();
   if (threadIdx.x == 0)
     for (int s = 0; s < PIPE_STAGES && t0 + s < t1; ++s) issue_tile<C>(p, A, t0 + s, ring + s * tile_elems, &bars[s]);
-  const int n = threadIdx.x % N;          // fixed output column of this thread
-  const int row_step = blockDim.x / N;
-  const int row0 = threadIdx.x / N;
-  C scol[KMAX];
+  // NV consecutive output columns per thread (NV = 2: one 16-byte store per
+  // row and half the shared-memory reads per output)
+  const int NN = N / NV;
+  const int n = (threadIdx.x % NN) * NV;  // first output column of this thread
+  const int row_step = blockDim.x / NN;
+  const int row0 = threadIdx.x / NN;
+  C scol[NV][KMAX];
   int64_t cur_z = -1;
   for (int64_t i = 0; t0 + i < t1; ++i) {
     const int64_t t = t0 + i;
@@ -351,12 +354,15 @@ k_pair_pipe_cols(const __grid_constant__ PairTile p, const void* __restrict__ A_
     const uint32_t phase = (uint32_t)((i / PIPE_STAGES) & 1);
     const int64_t z = t / p.U, u = t - (t / p.U) * p.U;
     if (z != cur_z) {
-      const C* Bz = B + z * p.b_zstride + p.b_noff[n];
 #pragma unroll
-      for (int k = 0; k < KMAX; ++k) {
-        C v = (k < K) ? __ldg(Bz + p.b_koff[k < K ? k : 0]) : czero<R>();
-        if (p.conj_b) v = cconj(v);
-        scol[k] = v;
+      for (int j = 0; j < NV; ++j) {
+        const C* Bz = B + z * p.b_zstride + p.b_noff[n + j];
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k) {
+          C v = (k < K) ? __ldg(Bz + p.b_koff[k < K ? k : 0]) : czero<R>();
+          if (p.conj_b) v = cconj(v);
+          scol[j][k] = v;
+        }
       }
       cur_z = z;
     }
@@ -365,11 +371,25 @@ k_pair_pipe_cols(const __grid_constant__ PairTile p, const void* __restrict__ A_
     C* Ot = O + z * p.out_zstride + u * p.R * p.N;
     for (int row = row0; row < Rr; row += row_step) {
       const C* trow = tile + rowoff_s[row];
-      C acc = czero<R>();
+      C acc[NV];
+#pragma unroll
+      for (int j = 0; j < NV; ++j) acc[j] = czero<R>();
 #pragma unroll
       for (int k = 0; k < KMAX; ++k)
-        if (k < K) cfma(acc, trow[koff_s[k]], scol[k]);
-      Ot[(int64_t)row * N + n] = acc;
+        if (k < K) {
+          const C a = trow[koff_s[k]];
+#pragma unroll
+          for (int j = 0; j < NV; ++j) cfma(acc[j], a, scol[j][k]);
+        }
+      if constexpr (NV % 2 == 0 && sizeof(R) == 4) {
+#pragma unroll
+        for (int j = 0; j < NV; j += 2)
+          *reinterpret_cast<float4*>(Ot + (int64_t)row * N + n + j) =
+              make_float4(acc[j].x, acc[j].y, acc[j + 1].x, acc[j + 1].y);
+      } else {
+#pragma unroll
+        for (int j = 0; j < NV; ++j) Ot[(int64_t)row * N + n + j] = acc[j];
+      }
     }
     fence_proxy_async();
     __syncthreads();

@@ -46,7 +46,7 @@ def test_tc_pair_matches_oracle(r, k, n, B, ascale, bscale, f16, monkeypatch):
     pairs = [(p, j) for j, p in enumerate(shared_pos)]
     plan = PairPlan(dims, [4] * (k + n), pairs, dtype="complex64")
     K, N = 4 ** k, 4 ** n
-    if K * N >= 256:
+    if K * N >= 256 and K >= 8:                  # K <= 4 stays on the SIMT column kernel
         assert plan.kernel == "tcgen05-3xtf32"
     ta = torch.from_numpy(acc).cuda()
     sb = torch.from_numpy(np.ascontiguousarray(site[bits].reshape(B, -1))).cuda()
