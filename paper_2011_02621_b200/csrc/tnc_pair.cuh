@@ -261,6 +261,14 @@ k_pair_pipe(const __grid_constant__ PairTile p, const void* __restrict__ A_, con
             if (n < N) cfma(acc[n], a, srow[n]);
           k = (k + 1 == K) ? 0 : k + 1;
         }
+        if constexpr (sizeof(R) == 4 && NMAX % 2 == 0) {
+          if (N == NMAX && (reinterpret_cast<uintptr_t>(orow) & 15) == 0) {
+#pragma unroll
+            for (int n = 0; n < NMAX; n += 2)
+              *reinterpret_cast<float4*>(orow + n) = make_float4(acc[n].x, acc[n].y, acc[n + 1].x, acc[n + 1].y);
+            continue;
+          }
+        }
 #pragma unroll
         for (int n = 0; n < NMAX; ++n)
           if (n < N) orow[n] = acc[n];
