@@ -677,22 +677,41 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
       }
       if (++acc == TS) { acc = 0; aph ^= 1; }
     }
-  } else if (warp == TC_PROD_WARP && RS > 0 && lane == 0) {
+  } else if (warp == TC_PROD_WARP && RS > 0) {
     // ---------------- raw-ring producer: cp.async.bulk of each tile's segments ----------------
+    // the whole warp issues: lane j copies segments j, j+32, ... (segment offsets
+    // held in registers), so a tile of many small segments is not serialised
+    // behind one thread's issue loop
     const uint32_t seg_bytes = (uint32_t)(p.Lseg * 8);
+    const int nseg = (int)p.Kout;
+    int64_t so[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int j = lane + 32 * u;
+      so[u] = (p.segoff && j < nseg) ? p.segoff[j] : 0;
+    }
     int rs = -1;
     uint32_t rph = 1;
     for (int t = 0; t < ntiles; ++t) {
       if (++rs == RS) rs = 0;
       if (rs == 0) rph ^= 1;
-      TC_TRACE(12, t);
+      if (lane == 0) TC_TRACE(12, t);
       mbar_wait_spin(&rempty[rs], rph ^ 1);
-      TC_TRACE(13, t);
+      if (lane == 0) TC_TRACE(13, t);
       unsigned char* dst = rawring + (size_t)rs * tc_raw_bytes(p.K);
       const float2* src = p.a + tbase[t];
-      mbar_expect_tx(&rfull[rs], (uint32_t)(p.Kout * seg_bytes));
-      for (int64_t j = 0; j < p.Kout; ++j)
-        bulk_g2s(dst + j * seg_bytes, src + (p.segoff ? p.segoff[j] : 0), seg_bytes, &rfull[rs]);
+      if (lane == 0) mbar_expect_tx(&rfull[rs], (uint32_t)(p.Kout * seg_bytes));
+      __syncwarp();
+      if (nseg <= 64) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int j = lane + 32 * u;
+          if (j < nseg) bulk_g2s(dst + (size_t)j * seg_bytes, src + so[u], seg_bytes, &rfull[rs]);
+        }
+      } else {
+        for (int j = lane; j < nseg; j += 32)
+          bulk_g2s(dst + (size_t)j * seg_bytes, src + (p.segoff ? p.segoff[j] : 0), seg_bytes, &rfull[rs]);
+      }
     }
   }
   tc_fence_before();
