@@ -185,13 +185,18 @@ namespace tnc {
 // ---------------------------------------------------------------------------
 constexpr int PIPE_STAGES = 2;
 
+// called by all 32 lanes of warp 0: lane 0 arms the barrier, then lane j
+// issues segments j, j+32, ... (many small segments are not serialised
+// behind one thread's issue loop and its segment-offset loads)
 template <typename C>
 __device__ __forceinline__ void issue_tile(const PairTile& p, const C* A, int64_t t, C* dst, uint64_t* bar) {
+  const int lane = threadIdx.x & 31;
   const int64_t z = t / p.U, u = t - (t / p.U) * p.U;
   const int64_t base = tile_base(p, z, u);
   const uint32_t seg_bytes = (uint32_t)(p.Lseg * sizeof(C));
-  mbar_expect_tx(bar, (uint32_t)(p.Kout * seg_bytes));
-  for (int64_t j = 0; j < p.Kout; ++j) bulk_g2s(dst + j * p.Lseg, A + base + p.segoff[j], seg_bytes, bar);
+  if (lane == 0) mbar_expect_tx(bar, (uint32_t)(p.Kout * seg_bytes));
+  __syncwarp();
+  for (int64_t j = lane; j < p.Kout; j += 32) bulk_g2s(dst + j * p.Lseg, A + base + p.segoff[j], seg_bytes, bar);
 }
 
 template <typename R, int NMAX, int KMAX>
@@ -220,7 +225,7 @@ k_pair_pipe(const __grid_constant__ PairTile p, const void* __restrict__ A_, con
   }
   for (int k = threadIdx.x; k < K; k += blockDim.x) koff_s[k] = p.koff[k];
   __syncthreads();
-  if (threadIdx.x == 0)
+  if (threadIdx.x < 32)
     for (int s = 0; s < PIPE_STAGES && t0 + s < t1; ++s) issue_tile<C>(p, A, t0 + s, ring + s * tile_elems, &bars[s]);
   int64_t cur_z = -1;
   const int rot = (K >= 8) ? lane % K : 0;   // lane-rotated start in the shared index
@@ -304,7 +309,7 @@ k_pair_pipe(const __grid_constant__ PairTile p, const void* __restrict__ A_, con
     }
     fence_proxy_async();   // order this stage's generic reads before the async-proxy refill
     __syncthreads();       // everyone is done with this stage
-    if (threadIdx.x == 0 && t + PIPE_STAGES < t1)
+    if (threadIdx.x < 32 && t + PIPE_STAGES < t1)
       issue_tile<C>(p, A, t + PIPE_STAGES, ring + stage * tile_elems, &bars[stage]);
   }
 }
@@ -346,7 +351,7 @@ k_pair_pipe_cols(const __grid_constant__ PairTile p, const void* __restrict__ A_
   for (int k = threadIdx.x; k < K; k += blockDim.x) koff_s[k] = p.koff[k];
   for (int r = threadIdx.x; r < Rr; r += blockDim.x) rowoff_s[r] = p.rowoff[r];
   __syncthreads();
-  if (threadIdx.x == 0)
+  if (threadIdx.x < 32)
     for (int s = 0; s < PIPE_STAGES && t0 + s < t1; ++s) issue_tile<C>(p, A, t0 + s, ring + s * tile_elems, &bars[s]);
   // NV consecutive output columns per thread (NV = 2: one 16-byte store per
   // row and half the shared-memory reads per output)
@@ -401,7 +406,7 @@ k_pair_pipe_cols(const __grid_constant__ PairTile p, const void* __restrict__ A_
     }
     fence_proxy_async();
     __syncthreads();
-    if (threadIdx.x == 0 && t + PIPE_STAGES < t1)
+    if (threadIdx.x < 32 && t + PIPE_STAGES < t1)
       issue_tile<C>(p, A, t + PIPE_STAGES, ring + stage * tile_elems, &bars[stage]);
   }
 }
