@@ -1,5 +1,5 @@
 """Run one configs[1] sweep case (for ncu / quick timing):
-    python tools/pair_case.py R K_LEGS N_LEGS B [iters]"""
+    python tools/pair_case.py R K_LEGS N_LEGS B [iters] [seed|bench]"""
 import sys
 from pathlib import Path
 
@@ -12,7 +12,11 @@ from paper_2011_02621_b200.engine import PairPlan  # noqa: E402
 
 r, k, n, B = (int(x) for x in sys.argv[1:5])
 iters = int(sys.argv[5]) if len(sys.argv) > 5 else 5
-perm, dims, pairs = bench.case_layout(r, k, n, seed=0)
+# layout seed: 0, or "bench" for the sweep's own seed (the case index)
+seed = 0
+if len(sys.argv) > 6:
+    seed = bench.sweep_cases().index((r, k, n, B)) if sys.argv[6] == "bench" else int(sys.argv[6])
+perm, dims, pairs = bench.case_layout(r, k, n, seed=seed)
 K, N = 4 ** k, 4 ** n
 plan = PairPlan(dims, [4] * (k + n), pairs, dtype="complex64")
 acc = torch.randn(B * 2 ** r * K, dtype=torch.complex64, device="cuda")
