@@ -671,6 +671,32 @@ int build_pair_plan(tnc_pair_plan& P, int dtype, int a_rank, const int64_t* a_di
           for (int q = (int)inner.size() - 1; q >= 0; --q) { off += (r % a_dims[inner[q]]) * sa[inner[q]]; r /= a_dims[inner[q]]; }
           looff[r0] = off;
         }
+        // converter bank spreading: when kraw is XOR-linear within a chunk, pick
+        // per-row-bit k XORs so each half-warp's 16 rows hit 16 distinct 8-byte
+        // bank slots (row bit i alone, or row bit i plus one k bit)
+        {
+          const int64_t KC = tnc::tc_kc(K);
+          bool lin = (KC & (KC - 1)) == 0 && (int64_t)tckraw.size() == K;
+          for (int64_t q = 0; q < K && lin; ++q)
+            for (int64_t x = 0; x < KC && lin; ++x) lin = tckraw[q ^ x] == (tckraw[q] ^ tckraw[x]);
+          if (lin) {
+            uint32_t span = 1u;                  // GF(2) span of the chosen 4-bit slot vectors
+            auto add = [&](int u) {
+              uint32_t t2 = span;
+              for (int v = 0; v < 16; ++v) if ((span >> v) & 1) t2 |= 1u << (v ^ u);
+              span = t2;
+            };
+            for (int i = 0; i < 4; ++i) {
+              const int u = (int)((looff[1 << i] - looff[0]) & 15);
+              if (!((span >> u) & 1)) { add(u); continue; }
+              for (int jb = 0; (1 << jb) < KC; ++jb) {
+                const int w = (int)(tckraw[1 << jb] & 15);
+                if (!((span >> (u ^ w)) & 1)) { P.tc.kx_row[i] = 1 << jb; add(u ^ w); break; }
+              }
+            }
+            if (getenv("TNC_TC_NOXOR")) memset(P.tc.kx_row, 0, sizeof P.tc.kx_row);
+          }
+        }
         P.tc_ok = true;
       }
     }

@@ -53,6 +53,10 @@ struct TcDesc {
   int64_t Kout, Lseg;
   const int64_t* segoff;           // [Kout] segment offsets from the tile base
   const int32_t* kraw;             // [K]
+  // bank-conflict avoidance for the converters' staged-tile reads: row r of a
+  // half-warp reads chunk slot q from k = q ^ x(r), x(r) = XOR of kx_row[i] over
+  // the set bits i < 4 of r (host: 0 unless kraw is XOR-linear within a chunk)
+  int32_t kx_row[4];
   const int64_t* ho_lo;            // optional two-level row-block base tables:
   const int64_t* ho_hi;            //   base(m) = ho_hi[m / p_lo] + ho_lo[m % p_lo]
   int64_t p_lo;
@@ -417,6 +421,16 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
     const int r = (warp & 3) * 32 + lane;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     const float2* A = p.a + looff_s[r];
+    // staged-tile reads: slot q of this row comes from k = q ^ xk (see TcDesc::kx_row)
+    int xk = 0, xm = 0;
+    if (RS > 0) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        xm |= p.kx_row[i];
+        if ((r >> i) & 1) xk ^= p.kx_row[i];
+      }
+    }
+    const int32_t kx = RS > 0 ? kraw_s[xk] : 0;
     int j = 0;                                   // this group's chunk counter
     for (int t = grp; t < ntiles && grp < NG; t += NG) {
       const float2* raw = nullptr;
@@ -435,7 +449,7 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
           // per-row scale from the whole row (the raw stage holds the full 128 x K tile)
           float m = 0.f;
           for (int k = 0; k < K; ++k) {
-            const float2 x = raw[kraw_s[k]];
+            const float2 x = raw[kraw_s[k] ^ kx];
             m = fmaxf(m, fmaxf(fabsf(x.x), fabsf(x.y)));
           }
           sA = tc_f16_scale(m);
@@ -450,7 +464,22 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
         if (RS > 0) {
           const int32_t* kr = kraw_s + c * KC;
 #pragma unroll
-          for (int q = 0; q < KC; ++q) v[q] = raw[kr[q]];
+          for (int q = 0; q < KC; ++q) v[q] = raw[kr[q] ^ kx];
+          if (xm) {                              // undo the per-row slot permutation
+#pragma unroll
+            for (int b = 0; (1 << b) < KC; ++b) {
+              if ((xm >> b) & 1) {
+                const bool sw = (xk >> b) & 1;
+#pragma unroll
+                for (int q = 0; q < KC; ++q) {
+                  if (q & (1 << b)) continue;
+                  const float2 u0 = v[q], u1 = v[q | (1 << b)];
+                  v[q] = sw ? u1 : u0;
+                  v[q | (1 << b)] = sw ? u0 : u1;
+                }
+              }
+            }
+          }
         } else {
           const int64_t* ko = akoff_s + c * KC;
 #pragma unroll

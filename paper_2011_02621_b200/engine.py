@@ -32,6 +32,7 @@ host fallback: without ``libtnc.so`` or an sm_100 device the engine raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from math import prod
 from typing import Sequence
@@ -608,7 +609,12 @@ class PairPlan:
     @property
     def kernel(self) -> str:
         k = self.L.tnc_pair_plan_kernel(self._h)
-        return {NV.K_SKINNY: "tiled-permute", NV.K_GENERIC: "generic", NV.K_TC: "tcgen05-3xtf32"}.get(k, str(k))
+        if k == NV.K_TC:
+            # K = 16 runs the fp16-split operands (kind::f16) when the raw ring
+            # stages whole tiles; TNC_TC_F16=0 forces 3xTF32 (tnc_tc.cuh launch_tc)
+            f16 = self.K == 16 and not os.environ.get("TNC_TC_F16", "").startswith("0")
+            return "tcgen05-3xfp16" if f16 else "tcgen05-3xtf32"
+        return {NV.K_SKINNY: "tiled-permute", NV.K_GENERIC: "generic"}.get(k, str(k))
 
     def __call__(self, a, b, out, batch: int, a_zstride: int, b_zstride: int, out_zstride: int, stream=None):
         import torch

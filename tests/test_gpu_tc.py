@@ -47,7 +47,7 @@ def test_tc_pair_matches_oracle(r, k, n, B, ascale, bscale, f16, monkeypatch):
     plan = PairPlan(dims, [4] * (k + n), pairs, dtype="complex64")
     K, N = 4 ** k, 4 ** n
     if K * N >= 256 and K >= 8:                  # K <= 4 stays on the SIMT column kernel
-        assert plan.kernel == "tcgen05-3xtf32"
+        assert plan.kernel.startswith("tcgen05-3x")
     ta = torch.from_numpy(acc).cuda()
     sb = torch.from_numpy(np.ascontiguousarray(site[bits].reshape(B, -1))).cuda()
     out = torch.empty((B, size // K * N), dtype=torch.complex64, device="cuda")
@@ -56,6 +56,49 @@ def test_tc_pair_matches_oracle(r, k, n, B, ascale, bscale, f16, monkeypatch):
     ref = O.sweep_step(acc.astype(np.complex128), perm, r, k, site.astype(np.complex128), bits)
     err = rel_l2(out.cpu().numpy(), ref)
     assert err <= 2e-6, err
+
+
+@pytest.mark.parametrize("r,k,n,B,seed", [(12, 2, 2, 2, "bench:16,2,2,256"), (12, 2, 3, 2, "bench:16,2,3,16"),
+                                         (12, 3, 3, 1, "bench:16,3,3,16"), (12, 3, 1, 2, "bench:16,3,1,1")])
+@pytest.mark.parametrize("noxor", [False, True])
+def test_tc_pair_sweep_layouts(r, k, n, B, seed, noxor, monkeypatch):
+    """k_tc_c64 on the sweep's own leg permutations (bench.case_layout seeds), whose
+    staged-tile reads use the per-row k-slot XOR (TcDesc::kx_row) -- and with it off"""
+    import torch
+
+    import bench
+    from paper_2011_02621_b200.engine import PairPlan
+
+    if noxor:
+        monkeypatch.setenv("TNC_TC_NOXOR", "1")
+    case = tuple(int(x) for x in seed.split(":")[1].split(","))
+    perm, dims, pairs = bench.case_layout(case[0], case[1], case[2], bench.sweep_cases().index(case))
+    # keep the innermost legs (the tile's row/k bank pattern) and drop outer row legs
+    drop = case[0] - r
+    keep = [i for i, x in enumerate(perm) if not (x < case[0] and sum(1 for y in perm[:i] if y < case[0]) < drop)]
+    perm = [perm[i] for i in keep]
+    order = sorted(range(len(perm)), key=lambda i: perm[i])
+    rank = {i: j for j, i in enumerate(order)}
+    perm = [rank[i] for i in range(len(perm))]
+    dims = [2 if x < r else 4 for x in perm]
+    shared_pos = sorted((i for i, x in enumerate(perm) if x >= r), key=lambda i: perm[i])
+    pairs = [(p, j) for j, p in enumerate(shared_pos)]
+    rng = np.random.default_rng(7)
+    size = int(np.prod(dims))
+    acc = ((rng.standard_normal((B, size)) + 1j * rng.standard_normal((B, size))) / np.sqrt(2)).astype(np.complex64)
+    site = ((rng.standard_normal((2,) + (4,) * (k + n)) + 1j * rng.standard_normal((2,) + (4,) * (k + n))) / 2
+            ).astype(np.complex64)
+    bits = rng.integers(0, 2, B)
+    plan = PairPlan(dims, [4] * (k + n), pairs, dtype="complex64")
+    K, N = 4 ** k, 4 ** n
+    assert plan.kernel.startswith("tcgen05-3x")
+    ta = torch.from_numpy(acc).cuda()
+    sb = torch.from_numpy(np.ascontiguousarray(site[bits].reshape(B, -1))).cuda()
+    out = torch.empty((B, size // K * N), dtype=torch.complex64, device="cuda")
+    plan(ta, sb, out, B, size, K * N, size // K * N)
+    torch.cuda.synchronize()
+    ref = O.sweep_step(acc.astype(np.complex128), perm, r, k, site.astype(np.complex128), bits)
+    assert rel_l2(out.cpu().numpy(), ref) <= 2e-6
 
 
 def test_tc_engine_step_contiguous():
