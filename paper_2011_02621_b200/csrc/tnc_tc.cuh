@@ -265,6 +265,12 @@ __device__ __forceinline__ void tmem_st(uint32_t taddr, const uint32_t (&v)[LEN]
                  ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]));
   }
 }
+// one lane of a converged warp (warp-uniform operands stay in uniform registers)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t e;
+  asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}" : "=r"(e));
+  return e != 0;
+}
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // B' (hi, lo) for batch element z, written by threads [tid0, tid0 + nthr)
@@ -625,6 +631,10 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
     }
   } else if (warp == TC_MMA_WARP) {
     // ---------------- MMA issuer (A from TMEM, B from smem) ----------------
+    // The CTA owns all 512 columns, so its TMEM base is 0: a compile-time base
+    // keeps every MMA operand warp-uniform (no per-MMA register broadcasts)
+    if (tmem != 0u) __trap();
+    const uint32_t tmem = 0u;
     const uint32_t idesc = tf32_idesc(Nr);
     const uint32_t idesc16 = (1u << 4) | ((uint32_t)(Nr >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
     const uint32_t bhi = smem_u32(Bhi), blo = smem_u32(Blo);
@@ -667,7 +677,7 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
         mbar_wait_spin(&full[stage], ph);
         TC_TRACE(8, it);
         tc_fence_after();
-        if (F16 && lane == 0) {
+        if (F16 && elect_one()) {
           // chunk c = reals [2KC c, 2KC (c+1)) of K'; per 16-real k-step: one column group of 8
           const uint32_t SBO16 = (Kr / 8) * 128;
           const uint32_t ahi = tmem + A0 + (uint32_t)stage * ACOLS, alo = ahi + KC;
@@ -682,7 +692,7 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
           }
           umma_commit(&empty[stage]);
           if (c == nchunk - 1) umma_commit(&tfull[acc]);
-        } else if (!F16 && lane == 0) {
+        } else if (!F16 && elect_one()) {
           const uint32_t ahi = tmem + A0 + (uint32_t)stage * ACOLS, alo = ahi + 2 * KC;
           const uint64_t dbh0 = umma_desc(bhi + (uint32_t)(c * KC / 2) * 128, 128, SBO_B);
           const uint64_t dbl0 = umma_desc(blo + (uint32_t)(c * KC / 2) * 128, 128, SBO_B);

@@ -49,12 +49,23 @@ __global__ void __launch_bounds__(128, 1) k_bench(int niter, unsigned long long*
                      ::"r"(tmem), "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
       }
       else if (MODE == 3) mma_tf32_ts(tmem + (i & 1) * N, tmem + 256 + 8 * (i & 3), bd, idesc, i < 2 ? 0u : 1u);
-      else if (MODE >= 4) {
+      else if (MODE >= 4 && MODE <= 6) {
         // chunk-shaped: 12 MMAs per group of 12 iterations, commit(s) every 12
         mma_tf32_ts(tmem + ((i >> 1) & 1) * N, tmem + 256 + 8 * (i & 7), bd + ((i & 3) * 64), idesc, i < 4 ? 0u : 1u);
         if (MODE == 5 && (i % 12) == 11) { umma_commit(&bar2[0]); umma_commit(&bar2[1]); }
         if (MODE == 6 && (i % 24) == 23) { umma_commit(&bar2[0]); umma_commit(&bar2[1]); }
       }
+      if (MODE == 8 && (i % 12) == 11) {     // chunk round trip: 12 MMAs, commit, wait
+        mma_tf32_ts(tmem, tmem + 256, bd, idesc, 1u);
+        umma_commit(&bar2[2]);
+        mbar_wait_spin(&bar2[2], (uint32_t)((i / 12) & 1));
+      } else if (MODE == 8) mma_tf32_ts(tmem, tmem + 256, bd, idesc, acc);
+      if (MODE == 10) {                       // single-MMA round trip: mma, commit, wait
+        mma_tf32_ts(tmem, tmem + 256, bd, idesc, acc);
+        umma_commit(&bar2[2]);
+        mbar_wait_spin(&bar2[2], (uint32_t)(i & 1));
+      }
+      if (MODE == 9) mma_tf32_ts(tmem + (i & 3) * 32, tmem + 256, bd, idesc, i < 4 ? 0u : 1u);   // 4 independent accumulators
     }
     umma_commit(&bar);
     mbar_wait(&bar, 0);
@@ -67,6 +78,74 @@ __global__ void __launch_bounds__(128, 1) k_bench(int niter, unsigned long long*
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
+}
+
+// MMA chain (thread 0, N columns, A in TMEM) while warps 4-7 stream tcgen05.st
+// (ST=1) or tcgen05.ld (ST=2) into their own TMEM columns: does TMEM traffic
+// from other warps slow the MMA issue?
+template <int ST, int N>
+__global__ void __launch_bounds__(256, 1) k_contend(int niter, unsigned long long* out) {
+  __shared__ __align__(1024) unsigned char sm[40 * 1024];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  __shared__ volatile int stop;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 40 * 1024 / 4; i += blockDim.x) reinterpret_cast<float*>(sm)[i] = 0.f;
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); mbar_fence_init(); stop = 0; }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&slot)), "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = tf32_idesc(N);
+    const uint64_t bd = umma_desc(smem_u32(sm), 128, 512);
+    const unsigned long long t0 = clock64();
+    for (int i = 0; i < niter; ++i) mma_tf32_ts(tmem, tmem + 256, bd, idesc, i == 0 ? 0u : 1u);
+    umma_commit(&bar);
+    mbar_wait_spin(&bar, 0);
+    const unsigned long long t1 = clock64();
+    out[blockIdx.x] = t1 - t0;
+    stop = 1;
+  } else if (warp >= 4 && ST) {
+    const uint32_t lb = (uint32_t)((warp & 3) * 32) << 16;
+    uint32_t v[16];
+    for (int q = 0; q < 16; ++q) v[q] = threadIdx.x * q;
+    int it = 0;
+    while (!stop) {
+      const uint32_t col = 320 + (uint32_t)((it & 7) * 16);
+      if (ST == 1) { tmem_st<16>(tmem + lb + col, v); tmem_wait_st(); }
+      else { tmem_ld16(tmem + lb + col, v); tmem_wait_ld(); v[0] += 1; }
+      ++it;
+    }
+    if (v[0] == 12345) out[0] = 0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+template <int ST, int N>
+void run_contend(const char* name) {
+  unsigned long long* d;
+  cudaMalloc(&d, 148 * 8);
+  const int niter = 4096;
+  k_contend<ST, N><<<148, 256>>>(niter, d);
+  k_contend<ST, N><<<148, 256>>>(niter, d);
+  unsigned long long h[148];
+  cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+  cudaError_t e = cudaGetLastError();
+  double avg = 0;
+  for (int i = 0; i < 148; ++i) avg += h[i];
+  printf("%-28s N=%3d: %7.1f cycles/MMA %s\n", name, N, avg / 148 / niter, e == cudaSuccess ? "" : cudaGetErrorString(e));
+  cudaFree(d);
 }
 
 template <int MODE, int N>
@@ -107,5 +186,19 @@ int main() {
   run<5, 64>("tf32 ts commit/12", 8);
   run<6, 64>("tf32 ts commit/24", 8);
   run<5, 128>("tf32 ts commit/12", 8);
+  run<0, 16>("tf32 ts", 8);
+  run<0, 32>("tf32 ts", 8);
+  run<9, 16>("tf32 ts 4acc", 8);
+  run<9, 32>("tf32 ts 4acc", 8);
+  run<2, 16>("bf16 ts", 16);
+  run<2, 32>("bf16 ts", 16);
+  run<8, 16>("tf32 ts chunk+wait/12", 8);
+  run<8, 64>("tf32 ts chunk+wait/12", 8);
+  run_contend<0, 16>("tf32 ts, idle warps");
+  run_contend<1, 16>("tf32 ts, 4 warps tcgen05.st");
+  run_contend<2, 16>("tf32 ts, 4 warps tcgen05.ld");
+  run_contend<1, 64>("tf32 ts, 4 warps tcgen05.st");
+  run<10, 16>("tf32 ts 1 mma+commit+wait", 8);
+  run<10, 128>("tf32 ts 1 mma+commit+wait", 8);
   return 0;
 }
