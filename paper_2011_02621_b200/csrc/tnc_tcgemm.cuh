@@ -636,6 +636,10 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
     if (p.tma_out && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   } else if (warp == TG_MMA_WARP) {
     // ---------------- MMA issuer ----------------
+    // all 512 columns are this CTA's, so the TMEM base is 0: a compile-time base
+    // keeps the MMA operands warp-uniform (see k_tc_c64)
+    if (tmem != 0u) __trap();
+    const uint32_t tmem = 0u;
     const uint32_t idesc = F16 ? f16_idesc(2 * NT) : tf32_idesc(2 * NT);
     // ring positions kept as counters (no div/mod on the issue path: at F16
     // rates the issuer's own instruction latency is what starves the pipe)
@@ -656,7 +660,7 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
           mbar_wait_spin(&bfull[bs], bph);
         }
         tc_fence_after();
-        if (lane == 0) {
+        if (elect_one()) {
           const uint64_t bb = dB + (uint64_t)(bs * bstage16);
           const uint64_t b2h = bb, b1h = bb + bblk16, b2l = bb + 3 * bblk16, b1l = bb + 4 * bblk16;
           if constexpr (F16) {
