@@ -247,7 +247,7 @@ def run_sweep(args, rank, world, dev):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": (roof_t / t_kern), "traffic": None,
                      "peak_source": f"{peak_src} hbm_gbs / bf16_tflops (MEASURED_PEAKS.json)",
-                     "kernel": "all contraction launches of the sweep: tnc::k_tc_c64 (tcgen05: fp16-split at K=16, else 3xTF32; K >= 8, K*N >= 256) "
+                     "kernel": "all contraction launches of the sweep: tnc::k_tc_c64 (tcgen05 3xTF32, K >= 8, K*N >= 256) "
                                "and tnc::k_pair_pipe* (TMA-fed fused permute+contract SIMT); projections excluded",
                      "algorithmic": "per case (acc + out + 2*projected site) * 8 B; flops 8*B*2^r*4^k*4^n",
                      "kernel_share_of_step": t_kern / t_case, "tflops_achieved": flops_tot / t_kern / 1e12},

@@ -500,7 +500,9 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
             scale_pending = false;
           }
         }
+        if ((warp & 3) == 0 && c == 0) TC_TRACE(16, t);
         mbar_wait_spin(&empty[stage], ph ^ 1);
+        if ((warp & 3) == 0 && c == 0) TC_TRACE(10, t);
         tc_fence_after();
         const uint32_t col = A0 + (uint32_t)stage * ACOLS;
         if constexpr (F16) {
@@ -534,6 +536,7 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
           }
         }
         if (!(p.dbg & 512)) tmem_wait_st();
+        if ((warp & 3) == 0 && c == 0) TC_TRACE(17, t);
         tc_fence_before();
         mbar_arrive_warp(&full[stage]);
         if (RS > 0 && c == nchunk - 1) {
@@ -819,10 +822,11 @@ __host__ inline int launch_tc(TcDesc p, int64_t Z, cudaStream_t s) {
   int TS16, AS16;
   tc_tmem_plan(p.K, tc_npad(p.N), TS16, AS16, true);
   // (K = 16 only: one chunk per tile, so the row max comes from the values
-  // being converted; at K = 64 the extra pass over the staged tile measured
-  // slower than 3xTF32.  TNC_TC_F16=0 forces 3xTF32.)
+  // being converted.  Opt-in, TNC_TC_F16=1: once the MMA issue was made
+  // warp-uniform, 3xTF32 measured equal or faster on every K = 16 sweep case,
+  // without the per-z scale pre-pass and with the smaller error.)
   const char* e16 = getenv("TNC_TC_F16");
-  p.f16 = (kc == 16 && p.K == 16 && p.raw_stages > 0 && AS16 >= 2 && !(e16 && e16[0] == '0')) ? 1 : 0;
+  p.f16 = (kc == 16 && p.K == 16 && p.raw_stages > 0 && AS16 >= 2 && e16 && e16[0] == '1') ? 1 : 0;
   if (getenv("TNC_TC_VERBOSE"))
     fprintf(stderr, "launch_tc K=%lld N=%lld M=%lld Z=%lld f16=%d raw_stages=%d AS16=%d per=%lld grid=%lld Kout=%lld Lseg=%lld\n",
             (long long)p.K, (long long)p.N, (long long)p.M, (long long)Z, p.f16, p.raw_stages, AS16,
@@ -845,7 +849,7 @@ __host__ inline int launch_tc(TcDesc p, int64_t Z, cudaStream_t s) {
     const unsigned long long t0 = h[0];
     const char* names[18] = {"conv_pre_empty", "conv_got_empty", "conv_arrived", "epi_pre_tfull", "epi_got_tfull",
                              "epi_done", "mma_pre_tempty", "mma_got_tempty", "mma_got_full", "mma_committed",
-                             "conv_pre_raw", "conv_got_raw", "prod_pre_rempty", "prod_got_rempty",
+                             "conv_got_empty2", "conv_got_raw", "prod_pre_rempty", "prod_got_rempty",
                              "epi_ld_done", "epi_sts_done", "conv_lds_done", "conv_st_done"};
     for (int sl = 0; sl < 18; ++sl) {
       printf("%-16s", names[sl]);

@@ -610,9 +610,9 @@ class PairPlan:
     def kernel(self) -> str:
         k = self.L.tnc_pair_plan_kernel(self._h)
         if k == NV.K_TC:
-            # K = 16 runs the fp16-split operands (kind::f16) when the raw ring
-            # stages whole tiles; TNC_TC_F16=0 forces 3xTF32 (tnc_tc.cuh launch_tc)
-            f16 = self.K == 16 and not os.environ.get("TNC_TC_F16", "").startswith("0")
+            # 3xTF32 by default; TNC_TC_F16=1 selects the fp16-split operands
+            # (kind::f16) at K = 16 when the raw ring stages whole tiles (launch_tc)
+            f16 = self.K == 16 and os.environ.get("TNC_TC_F16", "").startswith("1")
             return "tcgen05-3xfp16" if f16 else "tcgen05-3xtf32"
         return {NV.K_SKINNY: "tiled-permute", NV.K_GENERIC: "generic"}.get(k, str(k))
 
