@@ -245,7 +245,8 @@ int launch_tiled_fn(KFN kern, const tnc::PairTile& p, int64_t batch, const void*
 
 template <typename R, typename KFN>
 int launch_pipe_fn(KFN kern, const tnc::PairTile& p, int64_t batch, const void* a, const void* b, void* out,
-                   cudaStream_t s, bool cols = false) {
+                   cudaStream_t s, bool cols = false, bool prod = false) {
+  const int threads = prod ? tnc::PIPE_THREADS : 256;
   using C = typename tnc::cplx<R>::T;
   const size_t smem = cols ? 128 + (size_t)tnc::PIPE_STAGES * p.Kout * p.Lseg * sizeof(C) + (size_t)64 * 4 + (size_t)p.R * 4 + 16
                            : 128 + (size_t)tnc::PIPE_STAGES * p.Kout * p.Lseg * sizeof(C)
@@ -258,12 +259,12 @@ int launch_pipe_fn(KFN kern, const tnc::PairTile& p, int64_t batch, const void* 
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
   if (per_sm < 1) per_sm = 1;
   const int64_t ctas = std::min<int64_t>(total, (int64_t)sms * per_sm);
   const int64_t per = (total + ctas - 1) / ctas;
   const int64_t grid = (total + per - 1) / per;
-  kern<<<(unsigned)grid, 256, smem, s>>>(p, a, b, out, total, per);
+  kern<<<(unsigned)grid, threads, smem, s>>>(p, a, b, out, total, per);
   return check_launch("tnc_contract_pair[pipe]");
 }
 
@@ -292,6 +293,13 @@ int launch_pair_tiled(const tnc::PairTile& p, int64_t batch, const void* a, cons
       if constexpr (sizeof(R) == 4) return launch_pipe_fn<R>(tnc::k_pair_pipe_cols<R, 64>, p, batch, a, b, out, s, true);
     }
     if (N <= 32) {
+      // K >= 8: producer-warp variant (mbarrier stage release, no CTA barrier per tile)
+      static const bool prod_ok = !(getenv("TNC_PIPE_PROD") && getenv("TNC_PIPE_PROD")[0] == '0');
+      if (prod_ok && K >= 8 && N <= 4) {
+        if (N <= 1) return launch_pipe_fn<R>(tnc::k_pair_pipe<R, 1, 0, true>, p, batch, a, b, out, s, false, true);
+        if (N <= 2) return launch_pipe_fn<R>(tnc::k_pair_pipe<R, 2, 0, true>, p, batch, a, b, out, s, false, true);
+        return launch_pipe_fn<R>(tnc::k_pair_pipe<R, 4, 0, true>, p, batch, a, b, out, s, false, true);
+      }
       if (N <= 1) return launch_pipe_fn<R>(tnc::k_pair_pipe<R, 1, 0>, p, batch, a, b, out, s);
       if (N <= 2) return launch_pipe_fn<R>(tnc::k_pair_pipe<R, 2, 0>, p, batch, a, b, out, s);
       if (N <= 4) return launch_pipe_fn<R>(tnc::k_pair_pipe<R, 4, 0>, p, batch, a, b, out, s);

@@ -182,6 +182,37 @@ def test_sweep_step_matches_oracle(r, k, n, B, dtype, tol):
     assert rel_l2(got, ref) <= tol
 
 
+@pytest.mark.parametrize("kdims,ndims", [((4, 4), ()), ((4, 4), (2,)), ((4, 4), (4,)), ((2, 4), (4,)),
+                                         ((4, 2, 2), (2, 2))])
+@pytest.mark.parametrize("dtype,tol", [("complex128", 1e-12), ("complex64", 1e-5)])
+def test_pipe_producer_variant(kdims, ndims, dtype, tol):
+    """K >= 8, N <= 4: the producer-warp k_pair_pipe (mbarrier stage release)
+    on a permuted accumulator with many tiles per CTA, against tensordot."""
+    import torch
+
+    from paper_2011_02621_b200.engine import contract_pair_device
+
+    rng = np.random.default_rng(len(kdims) * 10 + len(ndims))
+    r, B = 15, 3
+    legs = [2] * r + list(kdims)
+    perm = list(rng.permutation(len(legs)))
+    a_dims = [legs[x] for x in perm]
+    shared_pos = [perm.index(r + j) for j in range(len(kdims))]
+    b_dims = list(kdims) + list(ndims)
+    pairs = [(shared_pos[j], j) for j in range(len(kdims))]
+    cdt = np.complex64 if dtype == "complex64" else np.complex128
+    acc = (rng.standard_normal((B,) + tuple(a_dims)) + 1j * rng.standard_normal((B,) + tuple(a_dims))).astype(cdt)
+    site = (rng.standard_normal((B,) + tuple(b_dims)) + 1j * rng.standard_normal((B,) + tuple(b_dims))).astype(cdt)
+    tdt = torch.complex64 if dtype == "complex64" else torch.complex128
+    ta = torch.from_numpy(acc.reshape(B, -1)).to("cuda", tdt)
+    tb = torch.from_numpy(site.reshape(B, -1)).to("cuda", tdt)
+    out = contract_pair_device(ta, a_dims, tb, b_dims, pairs, batch=B, a_zstride=ta.shape[1], b_zstride=tb.shape[1])
+    got = out.cpu().numpy().astype(np.complex128)
+    ref = np.stack([np.tensordot(acc[z].astype(np.complex128), site[z].astype(np.complex128),
+                                 axes=(shared_pos, list(range(len(kdims))))).reshape(-1) for z in range(B)])
+    assert rel_l2(got, ref) <= tol
+
+
 def test_kernel_variants_agree(golden_amplitudes):
     """Forcing the generic kernel gives the same amplitudes as the tuned path."""
     from paper_2011_02621_b200 import AmplitudeEngine, parse_circuit
