@@ -60,6 +60,10 @@ struct TcDesc {
   const int64_t* ho_lo;            // optional two-level row-block base tables:
   const int64_t* ho_hi;            //   base(m) = ho_hi[m / p_lo] + ho_lo[m % p_lo]
   int64_t p_lo;
+  // 1: the epilogue stages each warp's 32 result rows (one full accumulator
+  // chunk: 2N == padded width <= 32, so the rows are one contiguous block)
+  // and writes them with one cp.async.bulk store, double-buffered per warp
+  int32_t bulk_out;
 };
 
 constexpr int TC_CONV_WARPS = 8;
@@ -151,9 +155,11 @@ __host__ __device__ inline int64_t tc_kc(int64_t K) { return K >= 16 ? 16 : K; }
 __host__ __device__ inline int64_t tc_npad(int64_t N) { return N <= 8 ? 8 : ((N + 7) / 8) * 8; }
 constexpr int TC_EPI_PITCH = 144;        // bytes per staged row (128 + 16 pad: conflict-free)
 __host__ __device__ inline int64_t tc_raw_bytes(int64_t K) { return 128 * K * 8; }
-__host__ __device__ inline int64_t tc_smem_bytes(int64_t K, int64_t N, int64_t per, int64_t rs) {
+constexpr int TC_EPI_BULK_BYTES = 2 * 4096;  // bulk_out: two 32-row x 128 B buffers per warp
+__host__ __device__ inline int64_t tc_epi_warp_bytes(int bulk) { return bulk ? TC_EPI_BULK_BYTES : 32 * TC_EPI_PITCH; }
+__host__ __device__ inline int64_t tc_smem_bytes(int64_t K, int64_t N, int64_t per, int64_t rs, int bulk = 0) {
   return 1024 + tc_b_bytes(K, tc_npad(N)) + K * 8 + K * 4 + 128 * 8 + 6 * TC_MAX_STAGES * 8 + 128 + per * 8
-         + TC_EPI_WARPS * 32 * TC_EPI_PITCH + 16 + rs * tc_raw_bytes(K);
+         + TC_EPI_WARPS * tc_epi_warp_bytes(bulk) + 16 + rs * tc_raw_bytes(K);
 }
 // TMEM plan: TS accumulators of Nr columns, AS A-chunk stages of 4*KC columns (hi + lo)
 // f16: A stages of 2*kc columns (two fp16 per column) and TC_SCALE_COLS
@@ -553,7 +559,9 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
     const int eg = (warp - TC_EPI_WARP0) >> 2;   // epilogue group (alternate tiles; TS even)
     const int q = warp & 3;                      // lane quarter
     const int r = q * 32 + lane;                 // tile row
-    unsigned char* stg = epi_stage + (eg * 4 + q) * 32 * TC_EPI_PITCH;
+    unsigned char* stg = epi_stage + (eg * 4 + q) * tc_epi_warp_bytes(p.bulk_out);
+    const bool bulk = p.bulk_out != 0;
+    int oblk = 0;                                // bulk_out: staging buffer parity
     // tile -> (z, row block) tracked incrementally (this group steps by 2 tiles)
     int64_t zt = (g0 + eg) / p.tiles_per_z, mb = (g0 + eg) - zt * p.tiles_per_z;
     int64_t inv2_z = -1;
@@ -605,6 +613,48 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) * inv * inv2);
         }
+        if (bulk) {
+          // rows of cols*4 bytes, packed: the warp's 32 rows are the contiguous
+          // output block otile[0 .. 32N).  Lane writes 16-byte piece m of its row
+          // in slot order j = m ^ x (x = the lane's position inside a 128-byte
+          // wavefront), so a quarter-warp's stores hit distinct banks; the
+          // register blocks are permuted with uniform conditional swaps
+          const int P = cols / 4;                        // 16-byte pieces per row (4 or 8)
+          const int x = P == 8 ? (lane & 7) : ((lane >> 1) & 3);
+#pragma unroll
+          for (int b = 0; b < 3; ++b) {
+            if ((1 << b) >= P) continue;
+            const bool sw = (x >> b) & 1;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              if (j >= P || (j & (1 << b))) continue;
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const uint32_t u0 = v[4 * j + e], u1 = v[4 * (j | (1 << b)) + e];
+                v[4 * j + e] = sw ? u1 : u0;
+                v[4 * (j | (1 << b)) + e] = sw ? u0 : u1;
+              }
+            }
+          }
+          unsigned char* sb = stg + (oblk & 1) * 4096;
+          ++oblk;
+          // the bulk store that last read this buffer (two tiles ago) is done reading
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (j < P)
+              *reinterpret_cast<uint4*>(sb + lane * (P * 16) + (j ^ x) * 16) =
+                  make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          fence_proxy_async();
+          __syncwarp();
+          if (lane == 0 && !(p.dbg & 1)) {
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                         ::"l"(otile), "r"(smem_u32(sb)), "r"((uint32_t)(32 * P * 16)) : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+          continue;
+        }
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           if (4 * j < cols)
@@ -632,6 +682,7 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
       }
       if (q == 0) TC_TRACE(5, t);
     }
+    if (bulk && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   } else if (warp == TC_MMA_WARP) {
     // ---------------- MMA issuer (A from TMEM, B from smem) ----------------
     // The CTA owns all 512 columns, so its TMEM base is 0: a compile-time base
@@ -801,15 +852,27 @@ __host__ inline int launch_tc(TcDesc p, int64_t Z, cudaStream_t s) {
   // raw ring (TMA bulk staging) when alignment allows and >= 2 stages fit
   p.raw_stages = 0;
   const bool aligned = (((uintptr_t)p.a) % 16 == 0) && ((p.a_zstride * 8) % 16 == 0);
-  if (p.raw_ok && aligned && !(p.dbg & 256)) {
-    int rs_max = 4;
-    if (const char* e = getenv("TNC_TC_RS")) rs_max = atoi(e);
-    for (int rs = rs_max & ~1; rs >= 2; rs -= 2)
-      if (tc_smem_bytes(p.K, p.N, per, rs) <= 227 * 1024) { p.raw_stages = rs; break; }
+  const bool use_raw = p.raw_ok && aligned && !(p.dbg & 256);
+  // bulk result stores: one full accumulator chunk per tile (2N = padded
+  // width <= 32) and 16-byte aligned warp blocks; TNC_TC_BULKOUT=0 turns it off
+  const char* ebo = getenv("TNC_TC_BULKOUT");
+  const bool want_bulk = tc_npad(p.N) == p.N && p.N <= 16 && !(ebo && ebo[0] == '0') &&
+                         ((uintptr_t)p.out) % 16 == 0 && (p.out_zstride * 8) % 16 == 0;
+  p.bulk_out = 0;
+  for (int bo = want_bulk ? 1 : 0; bo >= 0; --bo) {
+    p.raw_stages = 0;
+    if (use_raw) {
+      int rs_max = 4;
+      if (const char* e = getenv("TNC_TC_RS")) rs_max = atoi(e);
+      for (int rs = rs_max & ~1; rs >= 2; rs -= 2)
+        if (tc_smem_bytes(p.K, p.N, per, rs, bo) <= 227 * 1024) { p.raw_stages = rs; break; }
+      if (bo && p.raw_stages == 0) continue;     // the raw ring matters more than the store path
+    }
+    if (tc_smem_bytes(p.K, p.N, per, p.raw_stages, bo) <= 227 * 1024) { p.bulk_out = bo; break; }
   }
-  if (tc_smem_bytes(p.K, p.N, per, p.raw_stages) > 227 * 1024) return -1;
+  if (tc_smem_bytes(p.K, p.N, per, p.raw_stages, p.bulk_out) > 227 * 1024) return -1;
   p.nstages = 0;
-  const size_t smem = (size_t)tc_smem_bytes(p.K, p.N, per, p.raw_stages);
+  const size_t smem = (size_t)tc_smem_bytes(p.K, p.N, per, p.raw_stages, p.bulk_out);
   const int64_t grid = (total + per - 1) / per;     // one wave when per fits in smem
   if (grid <= 0) return 0;
   if (p.dbg & 128) {
@@ -828,8 +891,8 @@ __host__ inline int launch_tc(TcDesc p, int64_t Z, cudaStream_t s) {
   const char* e16 = getenv("TNC_TC_F16");
   p.f16 = (kc == 16 && p.K == 16 && p.raw_stages > 0 && AS16 >= 2 && e16 && e16[0] == '1') ? 1 : 0;
   if (getenv("TNC_TC_VERBOSE"))
-    fprintf(stderr, "launch_tc K=%lld N=%lld M=%lld Z=%lld f16=%d raw_stages=%d AS16=%d per=%lld grid=%lld Kout=%lld Lseg=%lld\n",
-            (long long)p.K, (long long)p.N, (long long)p.M, (long long)Z, p.f16, p.raw_stages, AS16,
+    fprintf(stderr, "launch_tc K=%lld N=%lld M=%lld Z=%lld bulk_out=%d f16=%d raw_stages=%d AS16=%d per=%lld grid=%lld Kout=%lld Lseg=%lld\n",
+            (long long)p.K, (long long)p.N, (long long)p.M, (long long)Z, p.bulk_out, p.f16, p.raw_stages, AS16,
             (long long)per, (long long)grid, (long long)p.Kout, (long long)p.Lseg);
   float* bsc = nullptr;
   if (p.f16) {

@@ -24,10 +24,12 @@ def rel_l2(got, ref):
     # fp16-split path: arbitrary operand scales and a wide per-row dynamic range
     (9, 2, 2, 3, 1e-25, 1e20), (8, 3, 2, 2, 3e12, 1e-9), (10, 2, 3, 2, 1e-22, 1e-8), (8, 3, 3, 2, 7e-3, 5e4)])
 @pytest.mark.parametrize("f16", ["0", "1"])
-def test_tc_pair_matches_oracle(r, k, n, B, ascale, bscale, f16, monkeypatch):
+@pytest.mark.parametrize("bulk", ["1", "0"])
+def test_tc_pair_matches_oracle(r, k, n, B, ascale, bscale, f16, bulk, monkeypatch):
     import torch
 
     monkeypatch.setenv("TNC_TC_F16", f16)          # opt-in fp16-split variant of k_tc_c64 (read per launch)
+    monkeypatch.setenv("TNC_TC_BULKOUT", bulk)     # N = 16 cases: bulk-store epilogue, or the STG path
 
     from paper_2011_02621_b200.engine import PairPlan
 
