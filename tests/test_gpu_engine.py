@@ -182,6 +182,35 @@ def test_sweep_step_matches_oracle(r, k, n, B, dtype, tol):
     assert rel_l2(got, ref) <= tol
 
 
+@pytest.mark.parametrize("r,kdims,ndims", [(15, (4,), (4, 4)), (15, (2, 2), (4, 2, 2)), (13, (4,), (4, 4, 4)),
+                                           (12, (4, 4), (4, 4)), (9, (4,), (4, 4)), (6, (4,), (4, 4))])
+def test_pipe_cols_variant(r, kdims, ndims):
+    """complex64, K <= 16, 16 <= N <= 64: the column-mapped k_pair_pipe_cols
+    (two columns per thread) on permuted accumulators, many tiles per CTA and
+    several z, against tensordot"""
+    import torch
+
+    from paper_2011_02621_b200.engine import contract_pair_device
+
+    rng = np.random.default_rng(r + 7 * len(ndims))
+    B = 3
+    legs = [2] * r + list(kdims)
+    perm = list(rng.permutation(len(legs)))
+    a_dims = [legs[x] for x in perm]
+    shared_pos = [perm.index(r + j) for j in range(len(kdims))]
+    b_dims = list(kdims) + list(ndims)
+    pairs = [(shared_pos[j], j) for j in range(len(kdims))]
+    acc = (rng.standard_normal((B,) + tuple(a_dims)) + 1j * rng.standard_normal((B,) + tuple(a_dims))).astype(np.complex64)
+    site = (rng.standard_normal((B,) + tuple(b_dims)) + 1j * rng.standard_normal((B,) + tuple(b_dims))).astype(np.complex64)
+    ta = torch.from_numpy(acc.reshape(B, -1)).cuda()
+    tb = torch.from_numpy(site.reshape(B, -1)).cuda()
+    out = contract_pair_device(ta, a_dims, tb, b_dims, pairs, batch=B, a_zstride=ta.shape[1], b_zstride=tb.shape[1])
+    got = out.cpu().numpy().astype(np.complex128)
+    ref = np.stack([np.tensordot(acc[z].astype(np.complex128), site[z].astype(np.complex128),
+                                 axes=(shared_pos, list(range(len(kdims))))).reshape(-1) for z in range(B)])
+    assert rel_l2(got, ref) <= 1e-5
+
+
 @pytest.mark.parametrize("kdims,ndims", [((4, 4), ()), ((4, 4), (2,)), ((4, 4), (4,)), ((2, 4), (4,)),
                                          ((4, 2, 2), (2, 2))])
 @pytest.mark.parametrize("dtype,tol", [("complex128", 1e-12), ("complex64", 1e-5)])
