@@ -385,6 +385,9 @@ k_pair_pipe_cols(const __grid_constant__ PairTile p, const void* __restrict__ A_
   const int row_step = blockDim.x / NN;
   const int row0 = threadIdx.x / NN;
   C scol[NV][KMAX];
+  int kof[KMAX];                          // shared-index offsets in registers (no per-row table reads)
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) kof[k] = (k < K) ? koff_s[k] : 0;
   int64_t cur_z = -1;
   for (int64_t i = 0; t0 + i < t1; ++i) {
     const int64_t t = t0 + i;
@@ -407,18 +410,7 @@ k_pair_pipe_cols(const __grid_constant__ PairTile p, const void* __restrict__ A_
     mbar_wait_spin(&bars[stage], phase);
     const C* tile = ring + stage * tile_elems;
     C* Ot = O + z * p.out_zstride + u * p.R * p.N;
-    for (int row = row0; row < Rr; row += row_step) {
-      const C* trow = tile + rowoff_s[row];
-      C acc[NV];
-#pragma unroll
-      for (int j = 0; j < NV; ++j) acc[j] = czero<R>();
-#pragma unroll
-      for (int k = 0; k < KMAX; ++k)
-        if (k < K) {
-          const C a = trow[koff_s[k]];
-#pragma unroll
-          for (int j = 0; j < NV; ++j) cfma(acc[j], a, scol[j][k]);
-        }
+    auto store = [&](int row, const C (&acc)[NV]) {
       if constexpr (NV % 2 == 0 && sizeof(R) == 4) {
 #pragma unroll
         for (int j = 0; j < NV; j += 2)
@@ -428,6 +420,42 @@ k_pair_pipe_cols(const __grid_constant__ PairTile p, const void* __restrict__ A_
 #pragma unroll
         for (int j = 0; j < NV; ++j) Ot[(int64_t)row * N + n + j] = acc[j];
       }
+    };
+    // two rows per iteration: twice the independent FMA chains and shared
+    // loads in flight (short-scoreboard and fixed-latency stalls dominated)
+    int row = row0;
+    for (; row + row_step < Rr; row += 2 * row_step) {
+      const C* tr0 = tile + rowoff_s[row];
+      const C* tr1 = tile + rowoff_s[row + row_step];
+      C acc0[NV], acc1[NV];
+#pragma unroll
+      for (int j = 0; j < NV; ++j) acc0[j] = acc1[j] = czero<R>();
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k)
+        if (k < K) {
+          const C a0 = tr0[kof[k]], a1 = tr1[kof[k]];
+#pragma unroll
+          for (int j = 0; j < NV; ++j) {
+            cfma(acc0[j], a0, scol[j][k]);
+            cfma(acc1[j], a1, scol[j][k]);
+          }
+        }
+      store(row, acc0);
+      store(row + row_step, acc1);
+    }
+    if (row < Rr) {
+      const C* trow = tile + rowoff_s[row];
+      C acc[NV];
+#pragma unroll
+      for (int j = 0; j < NV; ++j) acc[j] = czero<R>();
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k)
+        if (k < K) {
+          const C a = trow[kof[k]];
+#pragma unroll
+          for (int j = 0; j < NV; ++j) cfma(acc[j], a, scol[j][k]);
+        }
+      store(row, acc);
     }
     fence_proxy_async();
     __syncthreads();
