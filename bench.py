@@ -447,6 +447,85 @@ def run_syc53(args, rank, world, dev, depth=SYC_DEPTH):
     return res
 
 
+SYC_SLICED_DEPTH = SYC_DEPTH + 2
+# cut edges for the sliced depth-10 network (tools/syc_sliced.py: greedy over
+# bond dims <= 16, minimising the largest intermediate, then the multiplies)
+SYC_SLICED_CUTS = [(9, 14), (2, 9)]
+
+
+def run_syc53_sliced(args, rank, world, dev, depth=SYC_SLICED_DEPTH):
+    """One amplitude of the 53-qubit Sycamore circuit at ``depth`` cycles
+    through the reference's slicing scheme (network.py:385-455: cut edges fixed
+    per slice, slices summed): unsliced, the network needs 2^35-element
+    intermediates; with the two cut edges it runs as 64 slices of at most 2^31
+    elements, one slice per device pass, summed on the device.  With N ranks
+    the 64 slices are split over the ranks (distributed.sharded_amplitudes)
+    and one NCCL all-reduce sums them (strong scaling: one amplitude)."""
+    import torch
+
+    from paper_2011_02621_b200 import AmplitudeEngine, pattern_rqc, sycamore53_graph
+    from paper_2011_02621_b200.distributed import sharded_amplitudes
+
+    t0 = time.perf_counter()
+    graph, pats, _ = sycamore53_graph()
+    circ = pattern_rqc(graph, [pats[c] for c in "ABCDCDAB"], depth, seed=0)
+    eng = AmplitudeEngine(circ, dtype="complex64", max_rank=SYC_MAX_RANK, cuts=SYC_SLICED_CUTS,
+                          max_batch_elems=1, device=dev)
+    setup_s = time.perf_counter() - t0
+    ex, plan = eng.executor, eng.plan
+    rng = np.random.default_rng(100)
+    bits = rng.integers(0, 2, (1, 53)).astype(np.int32)
+    sel = eng.selectors(bits)
+    amp = torch.zeros(1, dtype=torch.complex64, device=dev)
+
+    def one_pass():
+        amp.zero_()
+        if world > 1:
+            sharded_amplitudes(ex, sel, 1, amp)
+        else:
+            eng.amplitudes_device(sel, 1, amp)
+
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        one_pass()
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(dev.index) as clk:
+        for e0, e1 in evs:
+            e0.record(stream)
+            one_pass()
+            e1.record(stream)
+        torch.cuda.synchronize(dev)
+    t = sum(e0.elapsed_time(e1) for e0, e1 in evs) * 1e-3
+    barrier(world)
+    t_max = allreduce_max(t, world, dev)
+    res = {
+        "value": args.steps / t_max, "unit": "amplitudes/s", "ms_per_step": 1e3 * t_max / args.steps,
+        "scaling": "strong", "tflops_complex64_work": 8 * plan.multiplies * args.steps / t_max / 1e12,
+        "config": {"workload": f"configs[4] circuit family: 53-qubit Sycamore, ABCDCDAB, {depth} cycles, "
+                               f"sliced over cut edges {SYC_SLICED_CUTS} ({plan.slice_count} slices)",
+                   "dtype": "complex64", "bitstrings_per_step": 1, "slices": plan.slice_count,
+                   "multiplies_per_amplitude": plan.multiplies, "max_elems": plan.max_elems,
+                   "path_steps": len(plan.steps), "host_setup_s": setup_s,
+                   "sharding": ("slices split over ranks + one NCCL all_reduce(sum)" if world > 1
+                                else "single GPU, one slice per device pass, device slice sum"),
+                   "l2": "inputs larger than L2 (2 x 16 GiB ping-pong buffers)"},
+        "clocks": clk.summary(), "dtype": "complex64", "steps": args.steps, "warmup": args.warmup,
+    }
+    if args.e2e and world == 1:
+        outs = ["".join(map(str, row)) for row in bits]
+        t0 = time.perf_counter()
+        eng.amplitudes(outs, graph=False)
+        te = time.perf_counter() - t0
+        res["e2e"] = {"value": 1.0 / te, "unit": "amplitudes/s", "h2d_bytes_per_step": 53 * 4,
+                      "d2h_bytes_per_step": 8, "steps": 1,
+                      "path": "AmplitudeEngine.amplitudes(list of bitstring strings, graph=False) -> host complex array"}
+    res["_plan_steps"] = [(sp.M, sp.K, sp.N) for sp in plan.steps]
+    res["_slices"] = plan.slice_count
+    return res
+
+
 def syc_plan_shapes_host(depth=SYC_DEPTH):
     """(M, K, N) of every path step, computed on the host only (circuit, TNS
     evolution, path search, plan) -- for the CPU reference arm."""
@@ -683,7 +762,7 @@ def main():
     runner = {"sweep": run_sweep, "cfg0": run_cfg0, "syc53": run_syc53}[args.workload]
     res = runner(args, rank, world, dev)
     plan_steps = res.pop("_plan_steps", None)
-    syc = syc9 = None
+    syc = syc9 = syc10 = None
     if args.workload == "sweep" and args.syc:
         # the headline circuit family, measured beside the sweep: amplitudes/s of
         # the 53-qubit Sycamore network at the deepest depth one GPU holds
@@ -713,6 +792,19 @@ def main():
                                     "sample": f"numpy tensordot on 2^14-row samples of every distinct step shape, "
                                               f"{spent:.1f}s; scaled by rows (permutation cost not included)"}
         syc9["steps"], syc9["warmup"] = sargs9.steps, sargs9.warmup
+        # two cycles deeper, sliced (64 slices, 1.9e14 multiplies per amplitude)
+        gc.collect()
+        torch.cuda.empty_cache()
+        sargs10 = argparse.Namespace(**vars(sargs))
+        sargs10.steps, sargs10.warmup = 2, 1
+        syc10 = run_syc53_sliced(sargs10, rank, world, dev)
+        s10_steps, s10_slices = syc10.pop("_plan_steps", None), syc10.pop("_slices", 1)
+        if rank == 0 and args.cpu and world == 1 and s10_steps:
+            cv, spent = cpu_syc_rate(s10_steps, min(args.cpu_budget, 8.0))
+            syc10["cpu_baseline"] = {"value": cv / s10_slices, "unit": "amplitudes/s", "cores": _cpu_threads(),
+                                     "kind": "port",
+                                     "sample": f"numpy tensordot on 2^14-row samples of every distinct step shape, "
+                                               f"{spent:.1f}s; scaled by rows and by the {s10_slices} slices"}
     if rank == 0:
         if args.cpu and world == 1:
             if args.workload == "sweep":
@@ -732,6 +824,7 @@ def main():
         if syc is not None:
             line["amplitudes_53q"] = syc
             line["amplitudes_53q_depth9"] = syc9
+            line["amplitudes_53q_depth10_sliced"] = syc10
         print(json.dumps(line))
         if detail is not None:
             (ROOT / "gpurun_out").mkdir(exist_ok=True)
