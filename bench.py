@@ -250,7 +250,8 @@ def run_sweep(args, rank, world, dev):
                      "kernel": "all contraction launches of the sweep: tnc::k_tc_c64 (tcgen05 3xTF32, K >= 8, K*N >= 256) "
                                "and tnc::k_pair_pipe* (TMA-fed fused permute+contract SIMT); projections excluded",
                      "algorithmic": "per case (acc + out + 2*projected site) * 8 B; flops 8*B*2^r*4^k*4^n",
-                     "kernel_share_of_step": t_kern / t_case, "tflops_achieved": flops_tot / t_kern / 1e12},
+                     "kernel_share_of_step": t_kern / t_case, "tflops_achieved": flops_tot / t_kern / 1e12,
+                     "traffic_ncu": ncu_traffic_check()},
         "config": {"workload": "configs[1] pairwise-contraction sweep", "dtype": "complex64",
                    "cases": len(cases), "r": [16, 20, 24, 28], "k": [1, 2, 3], "n": [1, 2, 3],
                    "batch": [1, 16, 256], "operand_limit_elems": args.limit,
@@ -451,6 +452,33 @@ SYC_SLICED_DEPTH = SYC_DEPTH + 2
 # cut edges for the sliced depth-10 network (tools/syc_sliced.py: greedy over
 # bond dims <= 16, minimising the largest intermediate, then the multiplies)
 SYC_SLICED_CUTS = [(9, 14), (2, 9)]
+
+
+# ncu --set full captures committed under profiles/ (one launch each) and the
+# sweep case each was taken on: DRAM bytes per launch vs the algorithmic bytes
+NCU_TRAFFIC_PROFILE = "profiles/r01h_ncu_full_summary.json"
+NCU_TRAFFIC_CASES = [(16, 2, 2, 256), (24, 1, 2, 1)]
+
+
+def _ncu_bytes(v: str) -> float:
+    num, unit = v.split()
+    return float(num) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]
+
+
+def ncu_traffic_check():
+    """Per captured launch: dram read+write bytes (ncu) vs algorithmic bytes."""
+    try:
+        caps = json.loads((ROOT / NCU_TRAFFIC_PROFILE).read_text())
+    except (OSError, ValueError):
+        return None
+    out = []
+    for cap, case in zip(caps, NCU_TRAFFIC_CASES):
+        k = cap[0]
+        dram = _ncu_bytes(k["dram__bytes_read.sum"]) + _ncu_bytes(k["dram__bytes_write.sum"])
+        alg = case_traffic(*case)[0]
+        out.append({"kernel": k["kernel"].split("(")[0], "case": "r%d/k%d/n%d/B%d" % case, "dram_bytes": dram,
+                    "algorithmic_bytes": alg, "ratio": dram / alg, "source": NCU_TRAFFIC_PROFILE})
+    return out
 
 
 def run_syc53_sliced(args, rank, world, dev, depth=SYC_SLICED_DEPTH):
