@@ -270,7 +270,11 @@ def run_sweep(args, rank, world, dev):
 def sweep_e2e(args, cases, plans, inputs, dev, world):
     """Same sweep through the public API with host buffers: per case the
     accumulator and projection bits go H2D from pinned memory, gather +
-    contract run, the result comes back D2H; all inside the timed region."""
+    contract run, the result comes back D2H; all inside the timed region.
+    The cases are pipelined over three streams (H2D copies, compute, D2H
+    copies) with BENCH_E2E_SLOTS (4) device slots per buffer, so later cases'
+    uploads and earlier cases' downloads overlap case i's kernels (PCIe is
+    full duplex)."""
     import torch
 
     from paper_2011_02621_b200.engine import project_variants
@@ -278,25 +282,46 @@ def sweep_e2e(args, cases, plans, inputs, dev, world):
     max_acc = max(B * 2 ** r * 4 ** k for r, k, n, B in cases)
     max_out = max(B * 2 ** r * 4 ** n for r, k, n, B in cases)
     h_acc = torch.randn(max_acc, dtype=torch.complex64).pin_memory()
-    h_out = torch.empty(max_out, dtype=torch.complex64).pin_memory()
-    d_acc = torch.empty(max_acc, dtype=torch.complex64, device=dev)
-    d_out = torch.empty(max_out, dtype=torch.complex64, device=dev)
+    ns = int(os.environ.get("BENCH_E2E_SLOTS", "4"))
+    h_out = [torch.empty(max_out, dtype=torch.complex64).pin_memory() for _ in range(ns)]
+    d_acc = [torch.empty(max_acc, dtype=torch.complex64, device=dev) for _ in range(ns)]
+    d_out = [torch.empty(max_out, dtype=torch.complex64, device=dev) for _ in range(ns)]
     h_bits = [inputs[i][1].cpu().pin_memory() for i in range(len(cases))]
     stream = torch.cuda.current_stream(dev)
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     h2d = d2h = 0
     for r, k, n, B in cases:
         h2d += B * 2 ** r * 4 ** k * 8 + B * 4
         d2h += B * 2 ** r * 4 ** n * 8
 
     def step():
+        nc = len(cases)
+        ev_in = [torch.cuda.Event() for _ in range(nc)]
+        ev_comp = [torch.cuda.Event() for _ in range(nc)]
+        ev_out = [torch.cuda.Event() for _ in range(nc)]
+        s_in.wait_stream(stream)
         for ci, (r, k, n, B) in enumerate(cases):
             variants, bits, site = inputs[ci]
             na, no = B * 2 ** r * 4 ** k, B * 2 ** r * 4 ** n
-            d_acc[:na].copy_(h_acc[:na], non_blocking=True)
-            bits.copy_(h_bits[ci], non_blocking=True)
+            slot = ci % ns
+            with torch.cuda.stream(s_in):
+                if ci >= ns:
+                    s_in.wait_event(ev_comp[ci - ns])       # slot's accumulator consumed
+                d_acc[slot][:na].copy_(h_acc[:na], non_blocking=True)
+                bits.copy_(h_bits[ci], non_blocking=True)
+                ev_in[ci].record(s_in)
+            stream.wait_event(ev_in[ci])
+            if ci >= ns:
+                stream.wait_event(ev_out[ci - ns])          # slot's result downloaded
             project_variants(variants, bits, site, 4 ** (k + n), stream)
-            plans[ci](d_acc, site, d_out, B, 2 ** r * 4 ** k, 4 ** (k + n), 2 ** r * 4 ** n, stream)
-            h_out[:no].copy_(d_out[:no], non_blocking=True)
+            plans[ci](d_acc[slot], site, d_out[slot], B, 2 ** r * 4 ** k, 4 ** (k + n), 2 ** r * 4 ** n, stream)
+            ev_comp[ci].record(stream)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev_comp[ci])
+                h_out[slot][:no].copy_(d_out[slot][:no], non_blocking=True)
+                ev_out[ci].record(s_out)
+        stream.wait_stream(s_out)
+        stream.wait_stream(s_in)
         torch.cuda.synchronize(dev)
 
     step()
@@ -311,7 +336,8 @@ def sweep_e2e(args, cases, plans, inputs, dev, world):
     t = allreduce_max(e0.elapsed_time(e1) * 1e-3, world, dev)
     units = sum(B for *_, B in cases) * steps * world
     return {"value": units / t, "unit": "bitstring-steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "steps": steps, "path": "PairPlan + project_variants on host-resident pinned buffers"}
+            "steps": steps, "path": "PairPlan + project_variants on host-resident pinned buffers, H2D / compute / "
+                                    "D2H on three streams, %d device slots" % ns}
 
 
 SYC_DEPTH = 8
