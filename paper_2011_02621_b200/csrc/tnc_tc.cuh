@@ -18,10 +18,30 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <cuda.h>
 #include <cuda_fp16.h>
 #include "tnc_common.cuh"
 
 namespace tnc {
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*tg_encode_fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+inline tg_encode_fn tg_encoder() {
+  static tg_encode_fn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<tg_encode_fn>(f);
+  }
+  return fn;
+}
 
 struct TcDesc {
   int64_t M, K, N;                 // rows per batch element (multiple of 128)
@@ -62,7 +82,9 @@ struct TcDesc {
   int64_t p_lo;
   // 1: the epilogue stages each warp's 32 result rows (one full accumulator
   // chunk: 2N == padded width <= 32, so the rows are one contiguous block)
-  // and writes them with one cp.async.bulk store, double-buffered per warp
+  // and writes them with one cp.async.bulk store, double-buffered per warp;
+  // 2: N >= 32 (2N == padded width, several 32-column chunks): each chunk's
+  // 32 rows x 128 B go out as one TMA tensor-store box (tmO: [Z][M][2N] fp32)
   int32_t bulk_out;
 };
 
@@ -159,7 +181,7 @@ constexpr int TC_EPI_BULK_BYTES = 2 * 4096;  // bulk_out: two 32-row x 128 B buf
 __host__ __device__ inline int64_t tc_epi_warp_bytes(int bulk) { return bulk ? TC_EPI_BULK_BYTES : 32 * TC_EPI_PITCH; }
 __host__ __device__ inline int64_t tc_smem_bytes(int64_t K, int64_t N, int64_t per, int64_t rs, int bulk = 0) {
   return 1024 + tc_b_bytes(K, tc_npad(N)) + K * 8 + K * 4 + 128 * 8 + 6 * TC_MAX_STAGES * 8 + 128 + per * 8
-         + TC_EPI_WARPS * tc_epi_warp_bytes(bulk) + 16 + rs * tc_raw_bytes(K);
+         + TC_EPI_WARPS * tc_epi_warp_bytes(bulk) + 128 + rs * tc_raw_bytes(K);
 }
 // TMEM plan: TS accumulators of Nr columns, AS A-chunk stages of 4*KC columns (hi + lo)
 // f16: A stages of 2*kc columns (two fp16 per column) and TC_SCALE_COLS
@@ -319,9 +341,12 @@ __device__ __forceinline__ void build_b(const TcDesc& p, int64_t z, float* Bhi, 
 }
 
 // KH = complex values per converter thread per chunk (KC / 2)
-template <int KH, bool F16>
+// TMO: N >= 32 results written as TMA tensor-store boxes (bulk_out == 2); a
+// separate instantiation, so the other kernels' code is unchanged (with the
+// store path compiled in, the N = 16 kernel measured 3-5% slower)
+template <int KH, bool F16, bool TMO = false>
 __global__ void __launch_bounds__(TC_THREADS, 1)
-k_tc_c64(const __grid_constant__ TcDesc p) {
+k_tc_c64(const __grid_constant__ TcDesc p, const __grid_constant__ CUtensorMap tmO) {
   static_assert(!F16 || KH == 8, "F16 needs 16-complex chunks");
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   constexpr int KC = 2 * KH;
@@ -360,7 +385,8 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bdone + 1);
   int64_t* tbase = reinterpret_cast<int64_t*>(bdone + 2);   // [per_cta] accumulator base of each tile
   unsigned char* epi_stage = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(tbase + p.per_cta) + 15) & ~(uintptr_t)15);   // [4 warps][32 rows][144 B]
+      TMO ? (reinterpret_cast<uintptr_t>(tbase + p.per_cta) + 127) & ~(uintptr_t)127    // TMA store boxes
+          : (reinterpret_cast<uintptr_t>(tbase + p.per_cta) + 15) & ~(uintptr_t)15);
 
   // global tile index g = z * tiles_per_z + m; this CTA owns [g0, g1)
   const int64_t g0 = blockIdx.x * p.per_cta;
@@ -649,8 +675,14 @@ k_tc_c64(const __grid_constant__ TcDesc p) {
           fence_proxy_async();
           __syncwarp();
           if (lane == 0 && !(p.dbg & 1)) {
-            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
-                         ::"l"(otile), "r"(smem_u32(sb)), "r"((uint32_t)(32 * P * 16)) : "memory");
+            if constexpr (TMO) {
+              asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];"
+                           ::"l"(reinterpret_cast<uint64_t>(&tmO)), "r"(c0), "r"((int)(grow - lane)), "r"((int)zt),
+                             "r"(smem_u32(sb)) : "memory");
+            } else {
+              asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                           ::"l"(otile), "r"(smem_u32(sb)), "r"((uint32_t)(32 * P * 16)) : "memory");
+            }
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
           continue;
@@ -831,7 +863,8 @@ __host__ inline int launch_tc(TcDesc p, int64_t Z, cudaStream_t s) {
     if (cudaFuncSetAttribute(k_tc_c64<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
         cudaFuncSetAttribute(k_tc_c64<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
         cudaFuncSetAttribute(k_tc_c64<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
-        cudaFuncSetAttribute(k_tc_c64<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
+        cudaFuncSetAttribute(k_tc_c64<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
+        cudaFuncSetAttribute(k_tc_c64<8, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
       return -1;
     attr_done = true;
   }
@@ -856,10 +889,28 @@ __host__ inline int launch_tc(TcDesc p, int64_t Z, cudaStream_t s) {
   // bulk result stores: one full accumulator chunk per tile (2N = padded
   // width <= 32) and 16-byte aligned warp blocks; TNC_TC_BULKOUT=0 turns it off
   const char* ebo = getenv("TNC_TC_BULKOUT");
-  const bool want_bulk = tc_npad(p.N) == p.N && p.N <= 16 && !(ebo && ebo[0] == '0') &&
-                         ((uintptr_t)p.out) % 16 == 0 && (p.out_zstride * 8) % 16 == 0;
+  const bool want_bulk = tc_npad(p.N) == p.N && !(ebo && ebo[0] == '0') &&
+                         ((uintptr_t)p.out) % 16 == 0 && (p.out_zstride * 8) % 16 == 0 &&
+                         (p.N <= 16 || (p.N % 16 == 0 && p.Z <= 0x7fffffff && p.M <= 0x7fffffff));
+  // N >= 32: tensor map over the result, [Z][M][2N] fp32, box 32 floats x 32 rows
+  CUtensorMap tmO;
+  memset(&tmO, 0, sizeof tmO);
+  bool tm_ok = false;
+  if (want_bulk && p.N > 16 && p.K == 16) {
+    tg_encode_fn enc = tg_encoder();
+    if (enc) {
+      const cuuint64_t gdim[3] = {(cuuint64_t)(2 * p.N), (cuuint64_t)p.M, (cuuint64_t)Z};
+      const cuuint64_t gstr[2] = {(cuuint64_t)(p.N * 8), (cuuint64_t)((Z == 1 ? p.M * p.N : p.out_zstride) * 8)};
+      const cuuint32_t box[3] = {32, 32, 1};
+      const cuuint32_t es[3] = {1, 1, 1};
+      tm_ok = Z == 1 || p.out_zstride >= p.M * p.N;
+      tm_ok = tm_ok && enc(&tmO, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, p.out, gdim, gstr, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    }
+  }
   p.bulk_out = 0;
-  for (int bo = want_bulk ? 1 : 0; bo >= 0; --bo) {
+  for (int bo = (want_bulk && (p.N <= 16 || tm_ok)) ? 1 : 0; bo >= 0; --bo) {
     p.raw_stages = 0;
     if (use_raw) {
       int rs_max = 4;
@@ -868,11 +919,11 @@ __host__ inline int launch_tc(TcDesc p, int64_t Z, cudaStream_t s) {
         if (tc_smem_bytes(p.K, p.N, per, rs, bo) <= 227 * 1024) { p.raw_stages = rs; break; }
       if (bo && p.raw_stages == 0) continue;     // the raw ring matters more than the store path
     }
-    if (tc_smem_bytes(p.K, p.N, per, p.raw_stages, bo) <= 227 * 1024) { p.bulk_out = bo; break; }
+    if (tc_smem_bytes(p.K, p.N, per, p.raw_stages, bo) <= 227 * 1024) { p.bulk_out = bo ? (p.N > 16 ? 2 : 1) : 0; break; }
   }
-  if (tc_smem_bytes(p.K, p.N, per, p.raw_stages, p.bulk_out) > 227 * 1024) return -1;
+  if (tc_smem_bytes(p.K, p.N, per, p.raw_stages, p.bulk_out != 0) > 227 * 1024) return -1;
   p.nstages = 0;
-  const size_t smem = (size_t)tc_smem_bytes(p.K, p.N, per, p.raw_stages, p.bulk_out);
+  const size_t smem = (size_t)tc_smem_bytes(p.K, p.N, per, p.raw_stages, p.bulk_out != 0);
   const int64_t grid = (total + per - 1) / per;     // one wave when per fits in smem
   if (grid <= 0) return 0;
   if (p.dbg & 128) {
@@ -890,6 +941,7 @@ __host__ inline int launch_tc(TcDesc p, int64_t Z, cudaStream_t s) {
   // without the per-z scale pre-pass and with the smaller error.)
   const char* e16 = getenv("TNC_TC_F16");
   p.f16 = (kc == 16 && p.K == 16 && p.raw_stages > 0 && AS16 >= 2 && e16 && e16[0] == '1') ? 1 : 0;
+  if (p.f16 && p.bulk_out == 2) p.bulk_out = 0;     // the tensor-store epilogue is a tf32-kernel instantiation
   if (getenv("TNC_TC_VERBOSE"))
     fprintf(stderr, "launch_tc K=%lld N=%lld M=%lld Z=%lld bulk_out=%d f16=%d raw_stages=%d AS16=%d per=%lld grid=%lld Kout=%lld Lseg=%lld\n",
             (long long)p.K, (long long)p.N, (long long)p.M, (long long)Z, p.bulk_out, p.f16, p.raw_stages, AS16,
@@ -900,11 +952,12 @@ __host__ inline int launch_tc(TcDesc p, int64_t Z, cudaStream_t s) {
     if (cudaMallocAsync(reinterpret_cast<void**>(&bsc), (size_t)Z * sizeof(float), s) != cudaSuccess) return -1;
     p.bscale = bsc;
     k_tc_bmax<<<(unsigned)std::min<int64_t>(Z, 4096), 128, 0, s>>>(p, bsc);
-    k_tc_c64<8, true><<<(unsigned)grid, TC_THREADS, smem, s>>>(p);
+    k_tc_c64<8, true><<<(unsigned)grid, TC_THREADS, smem, s>>>(p, tmO);
     cudaFreeAsync(bsc, s);
-  } else if (kc == 4) k_tc_c64<2, false><<<(unsigned)grid, TC_THREADS, smem, s>>>(p);
-  else if (kc == 8) k_tc_c64<4, false><<<(unsigned)grid, TC_THREADS, smem, s>>>(p);
-  else k_tc_c64<8, false><<<(unsigned)grid, TC_THREADS, smem, s>>>(p);
+  } else if (kc == 4) k_tc_c64<2, false><<<(unsigned)grid, TC_THREADS, smem, s>>>(p, tmO);
+  else if (kc == 8) k_tc_c64<4, false><<<(unsigned)grid, TC_THREADS, smem, s>>>(p, tmO);
+  else if (p.bulk_out == 2) k_tc_c64<8, false, true><<<(unsigned)grid, TC_THREADS, smem, s>>>(p, tmO);
+  else k_tc_c64<8, false><<<(unsigned)grid, TC_THREADS, smem, s>>>(p, tmO);
   if (p.dbg & 128) {
     unsigned long long h[18 * 64];
     cudaStreamSynchronize(s);

@@ -746,23 +746,7 @@ __host__ inline size_t tg_smem_bytes(int NT, int KC, int RS, int BS, int f16, in
          8 * (2 * TG_MAX_RS + 2 * TC_MAX_STAGES + 2 * TG_MAX_BS + 8) + 16 + 4 * cn;
 }
 
-typedef CUresult (*tg_encode_fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-inline tg_encode_fn tg_encoder() {
-  static tg_encode_fn fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
-    void* f = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<tg_encode_fn>(f);
-  }
-  return fn;
-}
+// tg_encode_fn / tg_encoder(): tnc_tc.cuh
 
 // Tensor map for the TMA-store epilogue: the result legs (free legs, new legs,
 // batch z) sorted by stride must nest densely; legs are merged into <= 5 map
