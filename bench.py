@@ -272,7 +272,7 @@ def sweep_e2e(args, cases, plans, inputs, dev, world):
     accumulator and projection bits go H2D from pinned memory, gather +
     contract run, the result comes back D2H; all inside the timed region.
     The cases are pipelined over three streams (H2D copies, compute, D2H
-    copies) with BENCH_E2E_SLOTS (4) device slots per buffer, so later cases'
+    copies) with BENCH_E2E_SLOTS (6) device slots per buffer, so later cases'
     uploads and earlier cases' downloads overlap case i's kernels (PCIe is
     full duplex)."""
     import torch
@@ -282,7 +282,7 @@ def sweep_e2e(args, cases, plans, inputs, dev, world):
     max_acc = max(B * 2 ** r * 4 ** k for r, k, n, B in cases)
     max_out = max(B * 2 ** r * 4 ** n for r, k, n, B in cases)
     h_acc = torch.randn(max_acc, dtype=torch.complex64).pin_memory()
-    ns = int(os.environ.get("BENCH_E2E_SLOTS", "4"))
+    ns = int(os.environ.get("BENCH_E2E_SLOTS", "6"))
     h_out = [torch.empty(max_out, dtype=torch.complex64).pin_memory() for _ in range(ns)]
     d_acc = [torch.empty(max_acc, dtype=torch.complex64, device=dev) for _ in range(ns)]
     d_out = [torch.empty(max_out, dtype=torch.complex64, device=dev) for _ in range(ns)]
