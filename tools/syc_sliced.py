@@ -27,7 +27,8 @@ CUTS = [(9, 14), (2, 9)]
 def engine(depth, cuts):
     graph, pats, _ = sycamore53_graph()
     circ = pattern_rqc(graph, [pats[c] for c in "ABCDCDAB"], depth, seed=0)
-    return AmplitudeEngine(circ, dtype="complex64", max_rank=12, cuts=cuts, max_batch_elems=1)
+    return AmplitudeEngine(circ, dtype="complex64", max_rank=12, cuts=cuts,
+                           max_batch_elems=int(os.environ.get("SYC_Z", "1")))
 
 
 def main():
