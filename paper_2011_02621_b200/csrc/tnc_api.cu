@@ -250,7 +250,7 @@ int launch_pipe_fn(KFN kern, const tnc::PairTile& p, int64_t batch, const void* 
   using C = typename tnc::cplx<R>::T;
   const size_t smem = cols ? 128 + (size_t)tnc::PIPE_STAGES * p.Kout * p.Lseg * sizeof(C) + (size_t)64 * 4 + (size_t)p.R * 4 + 16
                            : 128 + (size_t)tnc::PIPE_STAGES * p.Kout * p.Lseg * sizeof(C)
-                             + (size_t)p.K * (p.N + 1) * sizeof(C) + (size_t)p.K * 4 + 16;
+                             + (size_t)p.K * (p.N + 1) * sizeof(C) + (size_t)p.K * 4 + (size_t)p.R * 4 + 16;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return check_launch("tnc pair pipe: smem attribute");
   const int64_t total = batch * p.U;

@@ -218,6 +218,7 @@ k_pair_pipe(const __grid_constant__ PairTile p, const void* __restrict__ A_, con
   const int SP = (int)p.N + 1;
   C* S = ring + PIPE_STAGES * tile_elems;
   int32_t* koff_s = reinterpret_cast<int32_t*>(S + p.K * SP);
+  int32_t* rowoff_s = koff_s + p.K;            // tile row offsets (a global load per row stalled on long scoreboard)
   const C* A = reinterpret_cast<const C*>(A_);
   const C* B = reinterpret_cast<const C*>(B_);
   C* O = reinterpret_cast<C*>(O_);
@@ -235,6 +236,7 @@ k_pair_pipe(const __grid_constant__ PairTile p, const void* __restrict__ A_, con
     mbar_fence_init();
   }
   for (int k = threadIdx.x; k < K; k += blockDim.x) koff_s[k] = p.koff[k];
+  for (int64_t r = threadIdx.x; r < p.R; r += blockDim.x) rowoff_s[r] = p.rowoff[r];
   __syncthreads();
   if (!PROD && threadIdx.x < 32)
     for (int s = 0; s < PIPE_STAGES && t0 + s < t1; ++s) issue_tile<C>(p, A, t0 + s, ring + s * tile_elems, &bars[s]);
@@ -271,7 +273,7 @@ k_pair_pipe(const __grid_constant__ PairTile p, const void* __restrict__ A_, con
     const C* tile = ring + stage * tile_elems;
     C* Ot = O + z * p.out_zstride + u * p.R * p.N;
     for (int64_t r = threadIdx.x; r < p.R; r += CT) {
-      const C* trow = tile + p.rowoff[r];
+      const C* trow = tile + rowoff_s[r];
       C* orow = Ot + r * N;
       if constexpr (KMAX == 0) {
         // accumulator-resident: N <= NMAX outputs in registers
