@@ -105,6 +105,14 @@ __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t phase) {
       "bra WAIT_%=;\n\t"
       "DONE_%=:\n\t}" ::"r"(smem_u32(bar)), "r"(phase) : "memory");
 }
+// Kernel attributes (cudaFuncSetAttribute) are per device context: a launch
+// path sets them once per device it runs on, tracked in a per-call-site mask.
+inline bool attr_needed(uint64_t done_mask, int* dev_out = nullptr) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev_out) *dev_out = dev;
+  return !((done_mask >> (dev & 63)) & 1ull);
+}
 // Keep freed stream-ordered blocks in the device's default pool across
 // synchronizations (the default release threshold returns them to the OS at
 // every sync, and the next cudaMallocAsync would map memory again: ~1 ms).

@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(256)
 k_pair_tiled_acc(const __grid_constant__ PairTile p, const void* __restrict__ A_, const void* __restrict__ B_,
                  void* __restrict__ O_) {
   using C = typename cplx<R>::T;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
   C* tile = reinterpret_cast<C*>(smem_raw);
   C* S = tile + p.Kout * p.Lseg;
   int32_t* koff_s = reinterpret_cast<int32_t*>(S + p.K * p.N);
@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(256)
 k_pair_tiled_row(const __grid_constant__ PairTile p, const void* __restrict__ A_, const void* __restrict__ B_,
                  void* __restrict__ O_) {
   using C = typename cplx<R>::T;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
   C* tile = reinterpret_cast<C*>(smem_raw);
   C* S = tile + p.Kout * p.Lseg;
   int32_t* koff_s = reinterpret_cast<int32_t*>(S + p.K * p.N);
@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(PROD ? PIPE_THREADS : 256, 2)
 k_pair_pipe(const __grid_constant__ PairTile p, const void* __restrict__ A_, const void* __restrict__ B_,
             void* __restrict__ O_, int64_t tiles_total, int64_t tiles_per_cta) {
   using C = typename cplx<R>::T;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
   C* ring = reinterpret_cast<C*>(smem_raw + 128);
   const int64_t tile_elems = p.Kout * p.Lseg;
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(256, 1)
 k_pair_pipe_cols(const __grid_constant__ PairTile p, const void* __restrict__ A_, const void* __restrict__ B_,
                  void* __restrict__ O_, int64_t tiles_total, int64_t tiles_per_cta) {
   using C = typename cplx<R>::T;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
   C* ring = reinterpret_cast<C*>(smem_raw + 128);
   const int64_t tile_elems = p.Kout * p.Lseg;

@@ -858,15 +858,16 @@ __host__ inline bool tc_shape_ok(int64_t K, int64_t N, int64_t M) {
 
 // returns 0 if launched, -1 on launch error
 __host__ inline int launch_tc(TcDesc p, int64_t Z, cudaStream_t s) {
-  static bool attr_done = false;
-  if (!attr_done) {
+  static uint64_t attr_done = 0;
+  int adev = 0;
+  if (attr_needed(attr_done, &adev)) {
     if (cudaFuncSetAttribute(k_tc_c64<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
         cudaFuncSetAttribute(k_tc_c64<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
         cudaFuncSetAttribute(k_tc_c64<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
         cudaFuncSetAttribute(k_tc_c64<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess ||
         cudaFuncSetAttribute(k_tc_c64<8, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
       return -1;
-    attr_done = true;
+    attr_done |= 1ull << (adev & 63);
   }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);

@@ -998,12 +998,13 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
     if (const char* e = getenv("TNC_TG_ILV")) p.ilv = atoi(e);
     const int64_t grid = p.ilv ? std::min<int64_t>(sms, p.Z * p.tiles_m) : (p.items + p.per_cta - 1) / p.per_cta;
     const size_t smem = tg_smem_bytes(p.NT, KC, RS, BS, f16, cn, tma);
-    static bool attr = false;
-    if (!attr) {
+    static uint64_t attr = 0;
+    int adev = 0;
+    if (attr_needed(attr, &adev)) {
       cudaFuncSetAttribute(k_tc_gemm<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       cudaFuncSetAttribute(k_tc_gemm<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       cudaFuncSetAttribute(k_tc_gemm<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-      attr = true;
+      attr |= 1ull << (adev & 63);
     }
     const CUtensorMap& to = tma ? tmO : tm;
     if (f16) k_tc_gemm<16, true><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm, to);

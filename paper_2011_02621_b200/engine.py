@@ -279,48 +279,10 @@ class PathExecutor:
         spec = plan.spec
         L = NV.lib()
         stream = torch.cuda.current_stream(self.device).cuda_stream
-        # raw site tensors [V, dims...] on device in the engine dtype
         self.raw = {}
         self.nvar = {}
-        for q in spec.nodes:
-            t = sites[q]
-            if not isinstance(t, torch.Tensor):
-                t = torch.from_numpy(np.ascontiguousarray(t))
-            t = t.to(device=self.device, dtype=self.tdtype).contiguous()
-            dims = spec.site_dims(q)
-            if tuple(t.shape[1:]) != dims:
-                raise EngineError(f"site {q}: shape {tuple(t.shape)} != (V, {dims})")
-            self.raw[q] = t
-            self.nvar[q] = int(t.shape[0])
-        # per-step re-laid-out site blocks via the projection kernel
         self.step_sites = []
-        self.keep = []
-        for sp in plan.steps:
-            q = sp.node
-            legs = spec.legs[q]
-            sdims = spec.site_dims(q)
-            sstr = dict(zip(legs, _strides(sdims)))
-            ldims = [int(spec.edges[e]) for e in sp.site_layout]
-            V = self.nvar[q]
-            per_var = prod(sdims) if sdims else 1
-            new_per_var = prod(ldims) if ldims else 1
-            dst = torch.empty((V, new_per_var), dtype=self.tdtype, device=self.device)
-            d = NV.ProjectDesc()
-            d.dtype = self.code
-            d.conj = 0
-            d.Z = V
-            d.slices_per_b = 1
-            d.s0 = 0
-            _fill_site(d.site, self.raw[q].data_ptr(), 0, [])
-            d.site.zstride = per_var
-            d.out = dst.data_ptr()
-            d.out_zstride = new_per_var
-            d.nd = len(ldims)
-            for i, e in enumerate(sp.site_layout):
-                d.dim[i] = ldims[i]
-                d.src_stride[i] = sstr[e]
-            NV.check(L.tnc_project(C.byref(d), C.c_void_p(stream)), "site relayout")
-            self.step_sites.append((dst, new_per_var, _site_cut_info(plan, sp.site_layout, ldims)))
+        self.load_sites(sites, stream)
         # offset tables
         self.tables = []
         for sp in plan.steps:
@@ -342,6 +304,63 @@ class PathExecutor:
         self._graphs: dict = {}
         self._graph_seen: set = set()
         self._build_descs()
+
+    def load_sites(self, sites: dict, stream=None) -> None:
+        """(Re)load the raw site tensors [V, dims...] and re-lay them out per
+        step ([V, cut legs, shared legs, new legs]) with the projection kernel.
+        A reload with the same variant counts writes into the existing step
+        blocks, so descriptors (and captured graphs) stay valid."""
+        torch = self.torch
+        plan, spec = self.plan, self.plan.spec
+        L = NV.lib()
+        st = torch.cuda.current_stream(self.device) if stream is None else stream
+        sptr = st if isinstance(st, int) else st.cuda_stream
+        reload = bool(self.step_sites)
+        for q in spec.nodes:
+            t = sites[q]
+            if not isinstance(t, torch.Tensor):
+                t = torch.from_numpy(np.ascontiguousarray(t))
+            t = t.to(device=self.device, dtype=self.tdtype).contiguous()
+            dims = spec.site_dims(q)
+            if tuple(t.shape[1:]) != dims:
+                raise EngineError(f"site {q}: shape {tuple(t.shape)} != (V, {dims})")
+            if reload:
+                if int(t.shape[0]) != self.nvar[q]:
+                    raise EngineError(f"site {q}: {int(t.shape[0])} variants, executor holds {self.nvar[q]}")
+                self.raw[q].copy_(t)             # in place: pointers in descriptors / graphs stay valid
+                continue
+            self.raw[q] = t
+            self.nvar[q] = int(t.shape[0])
+        for i, sp in enumerate(plan.steps):
+            q = sp.node
+            legs = spec.legs[q]
+            sdims = spec.site_dims(q)
+            sstr = dict(zip(legs, _strides(sdims)))
+            ldims = [int(spec.edges[e]) for e in sp.site_layout]
+            V = self.nvar[q]
+            per_var = prod(sdims) if sdims else 1
+            new_per_var = prod(ldims) if ldims else 1
+            if reload:
+                dst = self.step_sites[i][0]
+            else:
+                dst = torch.empty((V, new_per_var), dtype=self.tdtype, device=self.device)
+            d = NV.ProjectDesc()
+            d.dtype = self.code
+            d.conj = 0
+            d.Z = V
+            d.slices_per_b = 1
+            d.s0 = 0
+            _fill_site(d.site, self.raw[q].data_ptr(), 0, [])
+            d.site.zstride = per_var
+            d.out = dst.data_ptr()
+            d.out_zstride = new_per_var
+            d.nd = len(ldims)
+            for j, e in enumerate(sp.site_layout):
+                d.dim[j] = ldims[j]
+                d.src_stride[j] = sstr[e]
+            NV.check(L.tnc_project(C.byref(d), C.c_void_p(sptr)), "site relayout")
+            if not reload:
+                self.step_sites.append((dst, new_per_var, _site_cut_info(plan, sp.site_layout, ldims)))
 
     def _build_descs(self):
         plan, spec = self.plan, self.plan.spec
@@ -410,6 +429,11 @@ class PathExecutor:
         torch = self.torch
         need = z * self.plan.max_elems
         if self._buf is None or self._buf[0].numel() < need:
+            # captured graphs hold the old accumulator pointers: drop them with
+            # the buffers they write (a replay would otherwise write freed memory)
+            self._graphs.clear()
+            self._graph_seen.clear()
+            self._buf = None
             self._buf = (torch.empty(need, dtype=self.tdtype, device=self.device),
                          torch.empty(need, dtype=self.tdtype, device=self.device))
         return self._buf
@@ -456,7 +480,8 @@ class PathExecutor:
             if graph:
                 acc_flag = 1 if (accumulate or s0 != slices.start) else 0
                 key = (b0, nb, s0, ns, acc_flag, amp.data_ptr(),
-                       tuple(self._selptr(sel, q, b0) for q in plan.path))
+                       tuple(self._selptr(sel, q, b0) for q in plan.path),
+                       None if self._buf is None else self._buf[0].data_ptr())
                 g = self._graphs.get(key)
                 if g is not None:                  # replay: the descriptors are baked in
                     with torch.cuda.stream(st):
@@ -597,7 +622,7 @@ class PairPlan:
             odims = [odims[p] for p in out_perm]
         self.out_dims = odims
         self.K = prod(self.a_dims[p[0]] for p in self.pairs) if self.pairs else 1
-        self.N = prod(odims[len(self.a_dims) - len(self.pairs):]) if odims else 1
+        self.N = prod(d for i, d in enumerate(self.b_dims) if i not in sb)
         h = C.c_void_p()
         NV.check(self.L.tnc_pair_plan_create(self.code, len(adims), adims.ctypes.data, len(bdims), bdims.ctypes.data,
                                              len(pa), pa.ctypes.data if len(pa) else None,

@@ -29,11 +29,13 @@ from .engine import (ContractionPlan, EngineError, NetworkSpec, PathExecutor,
                      contract_pair_device)
 from .pathfind import NetworkShape, PathSearchError, find_optimal_path, treewidth_bound
 from .tensor import Tensor
-from .tns import PHYS, TNSState, apply_single_qubit, evolve, init_state, two_sided_evolve
+from .tns import (PHYS, RankMismatch, TNSBatch, TNSState, apply_single_qubit, evolve, init_state, psi_batch,
+                  two_sided_evolve)
 
 __all__ = ["TensorNetwork", "CutPlan", "CutPlanError", "AmplitudeStats", "AmplitudeBatch",
            "build_overlap_network", "plan_cuts", "slice_network", "contract_along_path",
-           "compute_amplitude", "compute_amplitudes", "AmplitudeEngine", "PLANNER_STATE_BUDGET"]
+           "compute_amplitude", "compute_amplitudes", "AmplitudeEngine", "TwoSidedEngine",
+           "PLANNER_STATE_BUDGET"]
 
 PLANNER_STATE_BUDGET = 1_000_000
 
@@ -119,7 +121,7 @@ def _overlap_sites(phi: TNSState, psis: Sequence[TNSState], device, dtype):
     graph = phi.graph
     tdt = torch.complex64 if dtype == "complex64" else torch.complex128
     out = {}
-    B = len(psis)
+    B = psis.batch if isinstance(psis, TNSBatch) else len(psis)
     for q in range(graph.num_qubits):
         a = phi.tensors[q]
         edges = graph.node_edges(q)
@@ -127,9 +129,12 @@ def _overlap_sites(phi: TNSState, psis: Sequence[TNSState], device, dtype):
         # phi/psi aux axes in node_edges order
         pa = [0] + [a.axis(e) for e in edges]
         at = np.transpose(a.data, pa)
-        b0 = psis[0].tensors[q]
-        pb = [0] + [b0.axis(e) for e in edges]
-        bt = np.stack([np.transpose(p.tensors[q].data, pb) for p in psis])
+        if isinstance(psis, TNSBatch):
+            bt = psis.tensors[q]                      # [B, 2, bonds in node_edges order]
+        else:
+            b0 = psis[0].tensors[q]
+            pb = [0] + [b0.axis(e) for e in edges]
+            bt = np.stack([np.transpose(p.tensors[q].data, pb) for p in psis])
         ta = torch.from_numpy(np.ascontiguousarray(at)).to(device=device, dtype=tdt)
         tb = torch.from_numpy(np.ascontiguousarray(bt)).to(device=device, dtype=tdt)
         res = contract_pair_device(ta, at.shape, tb, bt.shape[1:], [(0, 0)],
@@ -510,6 +515,16 @@ def compute_amplitudes(circuit: Circuit, in_bits: str, out_bits: Sequence[str], 
         return AmplitudeBatch(amps, eng.path, eng.path_score, eng.cut_plan.slice_count,
                               eng.plan.peak_rank, eng.plan.multiplies, "projected",
                               (time.perf_counter() - t0) * 1e3)
+    try:
+        eng = TwoSidedEngine(circuit, in_bits, split_cycle=split_cycle, cuts=cuts, max_rank=max_rank,
+                             dtype=dtype, tolerance=tolerance, ref_bits=out_bits[0])
+        amps = eng.amplitudes(out_bits)
+        return AmplitudeBatch(amps, eng.path, eng.path_score, eng.cut_plan.slice_count, eng.plan.peak_rank,
+                              eng.plan.multiplies, "two-sided", (time.perf_counter() - t0) * 1e3,
+                              {"shape_groups": 1})
+    except (RankMismatch, _ShapeMismatch):
+        pass
+    # members whose bra networks differ in shape: one group (path, pass) per shape
     fused = fuse_single_qubit_gates(circuit)
     graph = fused.graph
     n = graph.num_qubits
@@ -547,3 +562,111 @@ def compute_amplitudes(circuit: Circuit, in_bits: str, out_bits: Sequence[str], 
             info = (path, score, plan.slice_count, cplan.peak_rank, cplan.multiplies)
     return AmplitudeBatch(amps, info[0], info[1], info[2], info[3], info[4], "two-sided",
                           (time.perf_counter() - t0) * 1e3, {"shape_groups": len(groups)})
+
+
+class _ShapeMismatch(RuntimeError):
+    pass
+
+
+class TwoSidedEngine:
+    """Prepared two-sided evaluation of <out_b|U|in> -- the reference's default
+    mode (``compute_amplitude`` with split_cycle < depth; tns.py:185-212,
+    network.py:294-344) for a batch of output bitstrings.
+
+    phi = cycles [0, split) on |in> is evolved once; the bra sides
+    U2^dag|out_b> of a whole batch are evolved together on the host
+    (``tns.psi_batch``: one stacked SVD per gate, the reference's compression
+    rule), so every member keeps the reference's bond dimensions.  The overlap
+    sites C_q[b] = sum_s A_q[s] (x) conj(B_q^b[s]) are built on the GPU; all
+    bitstrings x slices of the cut plan then run through one ``PathExecutor``
+    (site variant b = bitstring b).  Network shape, cut plan and path come from
+    ``ref_bits`` (default 0...0) and are the reference's for every bitstring
+    whose bra has the same bond dimensions (checked per batch; a mismatch
+    raises and ``compute_amplitudes`` falls back to per-shape groups).
+    """
+
+    def __init__(self, circuit: Circuit, in_bits: str | None = None, split_cycle=None, cuts=None,
+                 max_rank=None, dtype: str = "complex64", tolerance: float = 1e-12, device=None,
+                 max_batch_elems: int | None = None, path=None, ref_bits: str | None = None):
+        import torch
+
+        n = circuit.num_qubits
+        self.circuit = circuit
+        self.in_bits = "0" * n if in_bits is None else in_bits
+        self.dtype = dtype
+        self.tolerance = tolerance
+        fused = fuse_single_qubit_gates(circuit)
+        self.fused = fused
+        d = fused.depth
+        self.split = d // 2 if split_cycle is None else int(split_cycle)
+        if not 0 <= self.split <= d:
+            raise ValueError(f"split_cycle {self.split} outside [0, {d}]")
+        graph = fused.graph
+        self.phi = evolve(init_state(graph, self.in_bits), fused, range(0, self.split), "forward", tolerance)
+        ref = psi_batch(fused, ["0" * n if ref_bits is None else ref_bits], self.split, tolerance)
+        self.psi_bonds = dict(ref.bond_dims)
+        self.edges = {e: self.phi.bond_dims[e] * ref.bond_dims[e] for e in graph.edges}
+        shape_net = _ShapeNet(range(n), self.edges)
+        self.cut_plan = _resolve_cuts(shape_net, cuts, max_rank)
+        if path is None:
+            self.path, self.path_score = _path_for(shape_net, self.cut_plan, max_rank)
+        else:
+            self.path, self.path_score = list(path), None
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.legs = {q: graph.node_edges(q) for q in range(n)}
+        self.plan = ContractionPlan(NetworkSpec(list(range(n)), self.edges, self.legs), self.path,
+                                    self.cut_plan.cut_edges)
+        self.max_batch_elems = max_batch_elems
+        self._ex: dict = {}
+        self.last_host_s = 0.0
+
+    @property
+    def multiplies(self) -> int:
+        return self.plan.multiplies
+
+    def bra_batch(self, bitstrings: Sequence[str]) -> TNSBatch:
+        pb = psi_batch(self.fused, list(bitstrings), self.split, self.tolerance)
+        if pb.bond_dims != self.psi_bonds:
+            raise _ShapeMismatch("bra bond dimensions differ from the engine's network shape")
+        return pb
+
+    def prepare(self, bitstrings: Sequence[str]) -> PathExecutor:
+        """Evolve the bras of ``bitstrings`` (host), build their overlap sites on
+        the GPU and load them into the executor for this batch size."""
+        import time as _t
+
+        t0 = _t.perf_counter()
+        _bits_matrix(bitstrings, self.circuit.num_qubits)      # validation only
+        pb = self.bra_batch(bitstrings)
+        self.last_host_s = _t.perf_counter() - t0
+        sites = _overlap_sites(self.phi, pb, self.device, self.dtype)
+        B = len(bitstrings)
+        ex = self._ex.get(B)
+        if ex is None:
+            for k in list(self._ex):                   # one live executor: its buffers are large
+                del self._ex[k]
+            mbe = self.max_batch_elems
+            ex = self._ex[B] = PathExecutor(self.plan, sites, dtype=self.dtype, device=self.device,
+                                            max_batch_elems=mbe)
+            import torch
+            ar = torch.arange(B, dtype=torch.int32, device=self.device)
+            ex._tw_sel = {q: ar for q in range(self.circuit.num_qubits)}
+        else:
+            ex.load_sites(sites)
+        return ex
+
+    def run(self, ex: PathExecutor, B: int, amp=None, slices=None, accumulate=False, graph: bool = False):
+        """Contract the prepared batch (all slices, or ``slices``) into ``amp``."""
+        import torch
+
+        if amp is None:
+            amp = torch.zeros(B, dtype=ex.tdtype, device=self.device)
+        ex.run(ex._tw_sel, B, amp, slices=slices, accumulate=accumulate, graph=graph)
+        return amp
+
+    def amplitudes(self, bitstrings: Sequence[str], slices=None) -> np.ndarray:
+        """Host bitstrings in, host complex128 amplitudes out (sum over
+        ``slices``, default all slices of the cut plan)."""
+        ex = self.prepare(bitstrings)
+        amp = self.run(ex, len(bitstrings), slices=slices)
+        return amp.cpu().numpy().astype(np.complex128)
