@@ -48,11 +48,11 @@ struct GemmDesc {
   int32_t NT, tiles_n;           // complex columns per N tile (multiple of 16)
   int32_t KC, nchunk;            // complex K per chunk
   int32_t RS, BS;                // raw A stages, B stages
-  int32_t dbg, _pad0;            // TNC_TG_DEBUG: 1 = MMA-only timing (no operand waits), 2 = no epilogue, 4 = epilogue without stores
   const unsigned char* bp;       // [combo][tile_n][chunk][hi: -Bi|Br|Bi][lo: -Bi|Br|Bi][NT x KC] canonical
   int64_t bp_combo_stride;       // bytes per combo
   int32_t f16, cn_smem;          // 1: fp16 split operands (needs amax_in); c_noff staged in smem (int32)
-  int32_t blk_contig, _pad6;     // 1: every warp's 32 rows x 16 columns block is one contiguous 4 KB run
+  int32_t blk_contig, g3;        // blk_contig: every warp's 32 rows x 16 columns block is one contiguous 4 KB run;
+                                 // g3: 3M (Gauss) complex products, F16 wide tiles (k_tc_gemm<16, true, true>)
   int64_t row_stride;            // != 0: rows r..r+31 of a warp block sit at oc(r) + i * row_stride
   const float* amax_in;          // [Z] max |re|,|im| of acc[z] (F16 scale)
   float* amax_out;               // [Z] max |re|,|im| of out[z] (zeroed by the host), or null
@@ -67,17 +67,6 @@ struct GemmDesc {
   int32_t nf, c_rows_contig;
   int64_t f_dim[TNC_MAX_LEGS], f_cstride[TNC_MAX_LEGS];
   const int64_t* c_noff;         // [N]
-  // TMA-store epilogue (tma_out): each warp's 32 rows x 16 columns block is
-  // staged in smem in the box order of tensor map tmO and stored by one
-  // cp.async.bulk.tensor; o_roff / o_coff give the staging element offset of
-  // row r / column c, *_tdim / *_tmul map every leg digit to a map coordinate
-  int32_t tma_out, o_swz;
-  int32_t o_rank, nn;
-  int16_t o_roff[32], o_coff[16];
-  int8_t f_tdim[TNC_MAX_LEGS], n_tdim[TNC_MAX_LEGS];
-  int32_t f_tmul[TNC_MAX_LEGS], n_tmul[TNC_MAX_LEGS];
-  int64_t n_dim[TNC_MAX_LEGS];
-  int32_t z_tdim, z_tmul;
 };
 
 constexpr int TG_THREADS = 15 * 32;
@@ -104,6 +93,9 @@ __device__ __forceinline__ float f16_scale(float amax) {
   p = p < -126 ? -126 : (p > 127 ? 127 : p);
   return __uint_as_float((uint32_t)(p + 127) << 23);
 }
+// 3M operands add re and im before the split (|re + im| < 2 max), so their
+// scales leave one more bit of headroom
+__device__ __forceinline__ float op_scale(float amax, int g3) { return g3 ? 0.5f * f16_scale(amax) : f16_scale(amax); }
 __device__ __forceinline__ void split_f16(float y, uint16_t& h, uint16_t& l) {
   const __half hh = __float2half_rn(y);
   const __half ll = __float2half_rn(y - __half2float(hh));
@@ -181,10 +173,19 @@ __global__ void k_bprime(const __grid_constant__ GemmDesc p, int64_t combos) {
     unsigned char* base = const_cast<unsigned char*>(p.bp) + combo * p.bp_combo_stride + ((tn * p.nchunk + c) * 6) * bbytes;
     if constexpr (F16) {
       const uint32_t boff = (nl & 7) * 16 + (nl >> 3) * SBO + (kl >> 3) * 128 + (kl & 7) * 2;
-      const float t = f16_scale(p.bscale[combo]);
+      const float t = op_scale(p.bscale[combo], p.g3);
       uint16_t rh, rl, ih, il;
       split_f16(sv.x * t, rh, rl);
       split_f16(sv.y * t, ih, il);
+      if (p.g3) {
+        // 3M: [Br | Bi | Br + Bi] hi, then lo (each block used alone, N = NT)
+        uint16_t sh, sl;
+        split_f16((sv.x + sv.y) * t, sh, sl);
+        const uint16_t v[6] = {rh, ih, sh, rl, il, sl};
+#pragma unroll
+        for (int b = 0; b < 6; ++b) *reinterpret_cast<uint16_t*>(base + b * bbytes + boff) = v[b];
+        continue;
+      }
       const uint16_t v[6] = {(uint16_t)(ih ^ 0x8000u), rh, ih, (uint16_t)(il ^ 0x8000u), rl, il};
 #pragma unroll
       for (int b = 0; b < 6; ++b) *reinterpret_cast<uint16_t*>(base + b * bbytes + boff) = v[b];
@@ -208,33 +209,6 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
 }
 
 
-// TMA tensor store of one staged box (rank 1..5), committed as its own bulk group
-__device__ __forceinline__ void tma_store(const CUtensorMap* m, int rank, const int32_t (&c)[5], uint32_t src) {
-  const uint64_t mp = reinterpret_cast<uint64_t>(m);
-  switch (rank) {
-    case 1:
-      asm volatile("cp.async.bulk.tensor.1d.global.shared::cta.tile.bulk_group [%0, {%1}], [%2];"
-                   ::"l"(mp), "r"(c[0]), "r"(src) : "memory");
-      break;
-    case 2:
-      asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];"
-                   ::"l"(mp), "r"(c[0]), "r"(c[1]), "r"(src) : "memory");
-      break;
-    case 3:
-      asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];"
-                   ::"l"(mp), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(src) : "memory");
-      break;
-    case 4:
-      asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4}], [%5];"
-                   ::"l"(mp), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(src) : "memory");
-      break;
-    default:
-      asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];"
-                   ::"l"(mp), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(src) : "memory");
-  }
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-
 __device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
                                            uint32_t accumulate) {
   asm volatile(
@@ -248,11 +222,15 @@ __device__ __forceinline__ uint32_t f16_idesc(int n_real) {
   return (1u << 4) | ((uint32_t)(n_real >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
 
-template <int KC, bool F16>
+// G3 (3M, Gauss): three real products per complex product instead of four --
+// T1 = Ar Br, T2 = Ai Bi, T3 = (Ar + Ai)(Br + Bi) in three accumulators of NT
+// columns, re = T1 - T2, im = T3 - T1 - T2 in the epilogue: 9 instead of 12
+// N = NT MMA units per chunk (wide tiles, NT = 128, one accumulator stage)
+template <int KC, bool F16, bool G3 = false>
 __global__ void __launch_bounds__(TG_THREADS, 1)
-k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMap tmA,
-          const __grid_constant__ CUtensorMap tmO) {
+k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMap tmA) {
   static_assert(!F16 || KC == 16, "F16 mode needs 16-complex chunks (K = 16 per MMA)");
+  static_assert(!G3 || F16, "3M products run on the fp16-split operands");
   extern __shared__ __align__(128) unsigned char smem_dyn[];
   constexpr int RB = KC * 8;                       // raw row bytes (KC complex)
   constexpr uint32_t SWM = RB == 128 ? 7u : 3u;    // swizzle row-group mask (128B / 64B)
@@ -265,7 +243,8 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
   const uint32_t SBO_B = F16 ? (KC / 8) * 128 : (KC / 4) * 128;
   // TMEM: TS accumulators of [D_re NT | D_im NT], A stages of 4*KC (tf32) or
   // 2*KC (fp16: two values per column) columns
-  constexpr uint32_t ACOLS = F16 ? 2 * KC : 4 * KC;
+  constexpr uint32_t ACOLS = G3 ? 3 * KC : (F16 ? 2 * KC : 4 * KC);
+  constexpr int NACC = G3 ? 3 : 2;                 // accumulator blocks of NT columns per stage
   // warp roles: converters [0, CONVW), epilogue [CONVW, 12) in EPIG groups of
   // four (one per TMEM lane quadrant; groups split the columns), 12 MMA, 13/14
   // producers.  fp16 conversion is cheap, so F16 gives the epilogue 8 warps.
@@ -275,20 +254,20 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
   // narrow tiles (NT <= 32, short epilogue per item, latency-bound): the
   // epilogue groups alternate items instead of splitting columns, over four
   // accumulator stages
-  const bool alt = F16 && NT <= 32;
+  const bool alt = F16 && !G3 && NT <= 32;
   // NT = 128 (F16, one N tile for N = 128): a single accumulator stage
-  const int TS = alt ? 4 : (NT > 64 ? 1 : 2);
+  const int TS = alt ? 4 : (NT > 64 || G3 ? 1 : 2);
   // A-resident (ares): the whole converted 128 x K tile fits TMEM next to the
   // accumulators, so it is converted once per row tile and reused by all
   // tiles_n column tiles (stage = chunk; released after the last column tile)
-  const bool ares = F16 && p.tiles_n > 1 && TS * 2 * NT + nchunk * (int)ACOLS <= 512 && nchunk <= TC_MAX_STAGES;
-  const int AS = ares ? nchunk : min(TC_MAX_STAGES, (512 - TS * 2 * NT) / (int)ACOLS);
-  const uint32_t A0 = (uint32_t)(TS * 2 * NT);
+  const bool ares = F16 && !G3 && p.tiles_n > 1 && TS * 2 * NT + nchunk * (int)ACOLS <= 512 && nchunk <= TC_MAX_STAGES;
+  const int AS = ares ? nchunk : min(TC_MAX_STAGES, (512 - TS * NACC * NT) / (int)ACOLS);
+  const uint32_t A0 = (uint32_t)(TS * NACC * NT);
   // smem: raw A ring (1024-aligned stages: swizzle atoms), B ring, epilogue staging, barriers
   unsigned char* araw = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~uintptr_t(1023));
   unsigned char* bring = araw + (size_t)RS * RAW_BYTES;
   unsigned char* estage = bring + (size_t)BS * 6 * bbytes;   // 1024-aligned (stage sizes are KB multiples)
-  uint64_t* bar = reinterpret_cast<uint64_t*>(estage + (p.tma_out ? EPIW * 8192 : EPIW * 32 * TG_EPI_PITCH));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(estage + EPIW * 32 * TG_EPI_PITCH);
   uint64_t* rfull = bar;                           // [RS] TMA -> converters
   uint64_t* rempty = rfull + TG_MAX_RS;            // [RS] converters -> TMA
   uint64_t* afull = rempty + TG_MAX_RS;            // [AS] converters -> MMA
@@ -307,12 +286,18 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
   // items of this CTA: a contiguous range (ilv = 0), or whole row tiles
   // (groups of tiles_n items) dealt round-robin, so that at any moment the
   // CTAs stream neighbouring rows of A and of the result (DRAM page locality)
+  // ilv == 2: items dealt one by one round-robin (item it of CTA b is
+  // it * grid + b): the tiles_n column tiles of a row tile run on neighbouring
+  // CTAs at the same time, so the A row tile is read from DRAM about once and
+  // from L2 by the others (not with ares, which keeps a row tile per CTA)
   const int64_t G = p.Z * p.tiles_m;
   const int64_t w0 = p.ilv ? 0 : blockIdx.x * p.per_cta;
-  const int nitems = p.ilv ? (int)(((G - blockIdx.x + gridDim.x - 1) / gridDim.x) * p.tiles_n)
+  const int nitems = p.ilv == 2 ? (int)((p.items - blockIdx.x + gridDim.x - 1) / gridDim.x)
+                   : p.ilv ? (int)(((G - blockIdx.x + gridDim.x - 1) / gridDim.x) * p.tiles_n)
                            : (int)(min(w0 + p.per_cta, p.items) - w0);
   auto itemw = [&](int it) -> int64_t {
     if (!p.ilv) return w0 + it;
+    if (p.ilv == 2) return (int64_t)it * gridDim.x + blockIdx.x;
     const int g = it / p.tiles_n;
     return ((int64_t)g * gridDim.x + blockIdx.x) * p.tiles_n + (it - g * p.tiles_n);
   };
@@ -337,7 +322,7 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp < CONVW && !(p.dbg & 1)) {
+  if (warp < CONVW) {
     // ---------------- converters: raw smem -> tf32/fp16 hi/lo -> TMEM ----------------
     // warp w converts rows 32*(w%4).. (its TMEM lane quadrant); tf32: complex
     // [h*KC/2, (h+1)*KC/2) with h = w/4 (8 warps), F16: all KC complex (4 warps).
@@ -354,7 +339,7 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
       if (ares && !gstart(it)) continue;
       if constexpr (F16) {
         const int64_t zz = itemw(it) / per_z;
-        if (zz != sz) { sz = zz; sA = f16_scale(__ldg(p.amax_in + zz)); }
+        if (zz != sz) { sz = zz; sA = op_scale(__ldg(p.amax_in + zz), G3); }
       }
       for (int c = 0; c < nchunk; ++c, ++j) {
         mbar_wait_spin(&rfull[rstage], rph);
@@ -362,6 +347,7 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
         if constexpr (F16) {
           // 16 complex -> 16 Ar and 16 Ai values, hi/lo fp16, two per TMEM column
           uint32_t rh[KC / 2], ih[KC / 2], rl[KC / 2], il[KC / 2];
+          uint32_t sh[G3 ? KC / 2 : 1], sl[G3 ? KC / 2 : 1];
 #pragma unroll
           for (int q = 0; q < KC / 2; ++q) {
             const uint32_t off = (uint32_t)(r * RB + 16 * q);
@@ -370,15 +356,26 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
             asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w) : "r"(src + phys));
             split_f16x2(x.x * sA, x.z * sA, rh[q], rl[q]);   // re of complex 2q, 2q+1
             split_f16x2(x.y * sA, x.w * sA, ih[q], il[q]);   // im
+            if constexpr (G3) split_f16x2((x.x + x.y) * sA, (x.z + x.w) * sA, sh[q], sl[q]);   // re + im
           }
           mbar_wait_spin(&aempty[astage], aph ^ 1);
           tc_fence_after();
-          // stage layout: [Ar_hi 8 | Ai_hi 8 | Ar_lo 8 | Ai_lo 8] columns (16 k each)
+          // stage layout: [Ar_hi 8 | Ai_hi 8 | Ar_lo 8 | Ai_lo 8] columns (16 k each);
+          // 3M: [Ar_hi | Ai_hi | As_hi | Ar_lo | Ai_lo | As_lo]
           const uint32_t col = A0 + (uint32_t)astage * ACOLS;
-          tmem_st<KC / 2>(tmem + lane_base + col, rh);
-          tmem_st<KC / 2>(tmem + lane_base + col + 8, ih);
-          tmem_st<KC / 2>(tmem + lane_base + col + 16, rl);
-          tmem_st<KC / 2>(tmem + lane_base + col + 24, il);
+          if constexpr (G3) {
+            tmem_st<KC / 2>(tmem + lane_base + col, rh);
+            tmem_st<KC / 2>(tmem + lane_base + col + 8, ih);
+            tmem_st<KC / 2>(tmem + lane_base + col + 16, sh);
+            tmem_st<KC / 2>(tmem + lane_base + col + 24, rl);
+            tmem_st<KC / 2>(tmem + lane_base + col + 32, il);
+            tmem_st<KC / 2>(tmem + lane_base + col + 40, sl);
+          } else {
+            tmem_st<KC / 2>(tmem + lane_base + col, rh);
+            tmem_st<KC / 2>(tmem + lane_base + col + 8, ih);
+            tmem_st<KC / 2>(tmem + lane_base + col + 16, rl);
+            tmem_st<KC / 2>(tmem + lane_base + col + 24, il);
+          }
           tmem_wait_st();
           tc_fence_before();
           mbar_arrive_warp(&afull[astage]);
@@ -432,13 +429,11 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
     // staged n-major stores when the innermost result leg is a new leg (runs
     // of consecutive n are contiguous); per-row stores otherwise (then the
     // innermost result leg is a free leg: consecutive rows are contiguous)
-    const bool staged = !(p.dbg & 8) && (p.c_rows_contig || p.n_contig || (p.N > 1 && p.c_noff[1] == p.c_noff[0] + 1));
+    const bool staged = (p.c_rows_contig || p.n_contig || (p.N > 1 && p.c_noff[1] == p.c_noff[0] + 1));
     const int cfirst = alt ? 0 : eg * 16, cstep = alt ? 16 : 16 * EPIG;
     float inv = 1.f, inv2 = 1.f;
     int64_t inv_z = -1;
     const uint32_t stg_s = smem_u32(stg);
-    const uint32_t ostage_s = smem_u32(estage);
-    int oblk = 0;
     for (int it = alt ? eg : 0; it < nitems; it += alt ? EPIG : 1) {
       const int acc = it % TS;
       const uint32_t ph = (it / TS) & 1;
@@ -474,24 +469,35 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
           inv_z = z;
           // two exact power-of-two factors: their product can leave the fp32 range
           // when both tensors are tiny although every result is representable
-          inv = 1.f / f16_scale(__ldg(p.amax_in + z));
-          inv2 = 1.f / f16_scale(__ldg(p.bscale + gemm_combo(p, z)));
+          inv = 1.f / op_scale(__ldg(p.amax_in + z), G3);
+          inv2 = 1.f / op_scale(__ldg(p.bscale + gemm_combo(p, z)), G3);
         }
       }
       mbar_wait(&tfull[acc], ph);
       tc_fence_after();
-      const uint32_t tre = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * 2 * NT);
-      if ((p.dbg & 2) || cfirst >= NT) {         // debug: drain nothing / no columns for this group
+      const uint32_t tre = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * NACC * NT);
+      if (cfirst >= NT) {                         // no columns for this group
         tc_fence_before();
         mbar_arrive_warp(&tempty[acc]);
-        if (p.dbg & 2) continue;
       }
       float2* Orow = O + oc;
       for (int c0 = cfirst; c0 < NT; c0 += cstep) {
         uint32_t vr[16], vi[16];
         tmem_ld16(tre + c0, vr);
         tmem_ld16(tre + NT + c0, vi);
-        tmem_wait_ld();
+        if constexpr (G3) {
+          uint32_t v3[16];
+          tmem_ld16(tre + 2 * NT + c0, v3);
+          tmem_wait_ld();
+#pragma unroll
+          for (int jj = 0; jj < 16; ++jj) {        // re = T1 - T2, im = T3 - T1 - T2
+            const float t1 = __uint_as_float(vr[jj]), t2 = __uint_as_float(vi[jj]);
+            vr[jj] = __float_as_uint(t1 - t2);
+            vi[jj] = __float_as_uint(__uint_as_float(v3[jj]) - t1 - t2);
+          }
+        } else {
+          tmem_wait_ld();
+        }
         if (c0 + cstep >= NT) {
           tc_fence_before();
           mbar_arrive_warp(&tempty[acc]);
@@ -502,52 +508,6 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
           vmax = fmaxf(vmax, fmaxf(fabsf(a), fabsf(b)));
           vr[jj] = __float_as_uint(a);
           vi[jj] = __float_as_uint(b);
-        }
-        if (p.dbg & 4) continue;                 // debug: TMEM loads only
-        if (p.tma_out) {
-          if (n0 + c0 >= p.N) continue;
-          // double-buffered 4 KB staging per warp; the store that last read
-          // this buffer must have finished reading it
-          const uint32_t sb = ostage_s + (uint32_t)(warp - CONVW) * 8192u + (uint32_t)(oblk & 1) * 4096u;
-          ++oblk;
-          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-          __syncwarp();
-          const int ro = p.o_roff[lane];
-#pragma unroll
-          for (int jj = 0; jj < 16; ++jj) {
-            uint32_t e = (uint32_t)(ro + p.o_coff[jj]);
-            if (p.o_swz) e = (e & ~15u) | ((((e >> 1) & 7u) ^ ((e >> 4) & 7u)) << 1) | (e & 1u);
-            asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(sb + e * 8u), "f"(__uint_as_float(vr[jj])),
-                         "f"(__uint_as_float(vi[jj])) : "memory");
-          }
-          fence_proxy_async();
-          __syncwarp();
-          if (lane == 0) {
-            int32_t cr[5] = {0, 0, 0, 0, 0};
-            uint32_t f = (uint32_t)(mt * 128 + q * 32);
-            for (int jl = p.nf - 1; jl >= 0; --jl) {
-              const uint32_t dm = (uint32_t)p.f_dim[jl], qq = f / dm;
-              const int32_t add = (int32_t)(f - qq * dm) * p.f_tmul[jl];
-              f = qq;
-              switch (p.f_tdim[jl]) { case 0: cr[0] += add; break; case 1: cr[1] += add; break;
-                                      case 2: cr[2] += add; break; case 3: cr[3] += add; break; default: cr[4] += add; }
-            }
-            uint32_t nn_ = (uint32_t)(n0 + c0);
-            for (int jl = p.nn - 1; jl >= 0; --jl) {
-              const uint32_t dm = (uint32_t)p.n_dim[jl], qq = nn_ / dm;
-              const int32_t add = (int32_t)(nn_ - qq * dm) * p.n_tmul[jl];
-              nn_ = qq;
-              switch (p.n_tdim[jl]) { case 0: cr[0] += add; break; case 1: cr[1] += add; break;
-                                      case 2: cr[2] += add; break; case 3: cr[3] += add; break; default: cr[4] += add; }
-            }
-            {
-              const int32_t add = (int32_t)z * p.z_tmul;
-              switch (p.z_tdim) { case 0: cr[0] += add; break; case 1: cr[1] += add; break;
-                                  case 2: cr[2] += add; break; case 3: cr[3] += add; break; default: cr[4] += add; }
-            }
-            tma_store(&tmO, p.o_rank, cr, sb);
-          }
-          continue;
         }
         const int64_t nleft = p.N - (n0 + c0);
         const int ncols = nleft < 16 ? (int)nleft : 16;
@@ -633,14 +593,13 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
         if (lane == 0 && vmax > 0.f) atomicMax(reinterpret_cast<unsigned int*>(p.amax_out) + z, __float_as_uint(vmax));
       }
     }
-    if (p.tma_out && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   } else if (warp == TG_MMA_WARP) {
     // ---------------- MMA issuer ----------------
     // all 512 columns are this CTA's, so the TMEM base is 0: a compile-time base
     // keeps the MMA operands warp-uniform (see k_tc_c64)
     if (tmem != 0u) __trap();
     const uint32_t tmem = 0u;
-    const uint32_t idesc = F16 ? f16_idesc(2 * NT) : tf32_idesc(2 * NT);
+    const uint32_t idesc = F16 ? f16_idesc(G3 ? NT : 2 * NT) : tf32_idesc(2 * NT);
     // ring positions kept as counters (no div/mod on the issue path: at F16
     // rates the issuer's own instruction latency is what starves the pipe)
     int bs = 0, stage = 0, acc = 0, stage0 = 0;
@@ -650,20 +609,35 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
     for (int it = 0; it < nitems; ++it) {
       mbar_wait_spin(&tempty[acc], tph ^ 1);
       tc_fence_after();
-      const uint32_t dre = tmem + (uint32_t)(acc * 2 * NT);
+      const uint32_t dre = tmem + (uint32_t)(acc * NACC * NT);
       const bool gs = !ares || gstart(it), ge = !ares || gend(it);
       if (gs) { stage0 = stage; aph0 = aph; }
       else { stage = stage0; aph = aph0; }         // ares: the group's stages again, same phase
       for (int c = 0; c < nchunk; ++c) {
-        if (!(p.dbg & 1)) {
-          if (gs) mbar_wait_spin(&afull[stage], aph);
-          mbar_wait_spin(&bfull[bs], bph);
-        }
+        if (gs) mbar_wait_spin(&afull[stage], aph);
+        mbar_wait_spin(&bfull[bs], bph);
         tc_fence_after();
         if (elect_one()) {
           const uint64_t bb = dB + (uint64_t)(bs * bstage16);
           const uint64_t b2h = bb, b1h = bb + bblk16, b2l = bb + 3 * bblk16, b1l = bb + 4 * bblk16;
-          if constexpr (F16) {
+          if constexpr (G3) {
+            // blocks [Br | Bi | Bs] hi then lo; small terms first, then hi*hi
+            const uint32_t arh = tmem + A0 + (uint32_t)stage * ACOLS;
+            const uint32_t aih = arh + 8, ash = arh + 16, arl = arh + 24, ail = arh + 32, asl = arh + 40;
+            const uint64_t brh = bb, bih = bb + bblk16, bsh = bb + 2 * bblk16;
+            const uint64_t brl = bb + 3 * bblk16, bil = bb + 4 * bblk16, bsl = bb + 5 * bblk16;
+            const uint32_t first = c == 0 ? 0u : 1u;
+            const uint32_t d1 = dre, d2 = dre + (uint32_t)NT, d3 = dre + 2u * (uint32_t)NT;
+            mma_f16_ts(d1, arl, brh, idesc, first);
+            mma_f16_ts(d2, ail, bih, idesc, first);
+            mma_f16_ts(d3, asl, bsh, idesc, first);
+            mma_f16_ts(d1, arh, brl, idesc, 1u);
+            mma_f16_ts(d2, aih, bil, idesc, 1u);
+            mma_f16_ts(d3, ash, bsl, idesc, 1u);
+            mma_f16_ts(d1, arh, brh, idesc, 1u);
+            mma_f16_ts(d2, aih, bih, idesc, 1u);
+            mma_f16_ts(d3, ash, bsh, idesc, 1u);
+          } else if constexpr (F16) {
             const uint32_t arh = tmem + A0 + (uint32_t)stage * ACOLS;
             const uint32_t aih = arh + 8, arl = arh + 16, ail = arh + 24;
             const uint32_t first = c == 0 ? 0u : 1u;
@@ -698,7 +672,7 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
       }
       if (++acc == TS) { acc = 0; tph ^= 1; }
     }
-  } else if (warp == TG_APROD_WARP && lane == 0 && !(p.dbg & 1)) {
+  } else if (warp == TG_APROD_WARP && lane == 0) {
     // ---------------- A producer: TMA tiles into the group's raw slice ----------------
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     int j = 0, rs = 0;
@@ -715,7 +689,7 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
         if (++rs == RS) { rs = 0; rph ^= 1; }
       }
     }
-  } else if (warp == TG_BPROD_WARP && lane == 0 && !(p.dbg & 1)) {
+  } else if (warp == TG_BPROD_WARP && lane == 0) {
     // ---------------- B producer: Br/Bi hi/lo chunks ----------------
     int bi = 0, bs = 0;
     uint32_t bph = 0;
@@ -740,138 +714,16 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
   }
 }
 
-__host__ inline size_t tg_smem_bytes(int NT, int KC, int RS, int BS, int f16, int64_t cn = 0, int tma = 0) {
+__host__ inline size_t tg_smem_bytes(int NT, int KC, int RS, int BS, int f16, int64_t cn = 0) {
   return 1024 + (size_t)RS * 128 * KC * 8 + (size_t)BS * 6 * tg_block_bytes(NT, KC, f16) +
-         (size_t)(f16 ? 8 : 4) * (tma ? 8192 : 32 * TG_EPI_PITCH) +
+         (size_t)(f16 ? 8 : 4) * 32 * TG_EPI_PITCH +
          8 * (2 * TG_MAX_RS + 2 * TC_MAX_STAGES + 2 * TG_MAX_BS + 8) + 16 + 4 * cn;
 }
 
 // tg_encode_fn / tg_encoder(): tnc_tc.cuh
 
-// Tensor map for the TMA-store epilogue: the result legs (free legs, new legs,
-// batch z) sorted by stride must nest densely; legs are merged into <= 5 map
-// dimensions so that every warp block (32 rows x 16 columns, aligned) is one
-// box.  Fills the tma_out fields of p; false = keep the register/LSU stores.
-inline bool tg_out_map(const tnc_step_desc& d, GemmDesc& p, CUtensorMap& tm, tg_encode_fn enc) {
-  p.tma_out = 0;
-  // opt-in (TNC_TG_TMAOUT=1): measured slower than the LSU stores on the 53q
-  // steps (one in-flight box per warp buffer; strided 256-byte box rows)
-  {
-    const char* e = getenv("TNC_TG_TMAOUT");
-    if (!e || e[0] != '1') return false;
-  }
-  if (d.nn <= 0 || d.nn > TNC_MAX_LEGS || d.nf <= 0) return false;
-  if (d.M % 128 || d.N % 16 || p.NT % 16 || d.out_zstride != d.M * d.N) return false;
-  struct Leg { int64_t dim, stride, box; int kind, idx, tdim; int64_t mult; };
-  std::vector<Leg> legs;
-  auto pow2 = [](int64_t x) { return x > 0 && (x & (x - 1)) == 0; };
-  for (int j = 0; j < d.nf; ++j) {
-    if (!pow2(d.f_dim[j])) return false;
-    legs.push_back({d.f_dim[j], d.f_cstride[j], 1, 0, j, 0, 1});
-  }
-  for (int i = 0; i < d.nn; ++i) {
-    if (!pow2(d.n_dim[i])) return false;
-    legs.push_back({d.n_dim[i], d.n_cstride[i], 1, 1, i, 0, 1});
-  }
-  legs.push_back({d.Z, d.out_zstride, 1, 2, 0, 0, 1});
-  // block extents: 32 rows over the innermost free legs, 16 columns over the innermost new legs
-  {
-    int64_t rem = 32;
-    for (int j = d.nf - 1; j >= 0 && rem > 1; --j) { const int64_t e = std::min(d.f_dim[j], rem); legs[j].box = e; rem /= e; }
-    if (rem > 1) return false;
-    rem = 16;
-    for (int i = d.nn - 1; i >= 0 && rem > 1; --i) { const int64_t e = std::min(d.n_dim[i], rem); legs[d.nf + i].box = e; rem /= e; }
-    if (rem > 1) return false;
-  }
-  std::vector<int> ord;
-  for (int i = 0; i < (int)legs.size(); ++i) if (legs[i].dim > 1 || legs[i].box > 1) ord.push_back(i);
-  std::sort(ord.begin(), ord.end(), [&](int a, int b) { return legs[a].stride < legs[b].stride; });
-  if (ord.empty() || legs[ord[0]].stride != 1) return false;
-  for (size_t k = 1; k < ord.size(); ++k)
-    if (legs[ord[k]].stride != legs[ord[k - 1]].stride * legs[ord[k - 1]].dim) return false;
-  // merge into map dimensions
-  struct Dim { int64_t ext, stride, box; };
-  std::vector<Dim> dims;
-  for (int li : ord) {
-    Leg& L = legs[li];
-    if (!dims.empty()) {
-      Dim& c = dims.back();
-      if ((L.box == 1 || c.box == c.ext) && c.ext * L.dim < (1LL << 31)) {
-        L.tdim = (int)dims.size() - 1;
-        L.mult = c.ext;
-        c.box *= L.box;
-        c.ext *= L.dim;
-        continue;
-      }
-    }
-    L.tdim = (int)dims.size();
-    L.mult = 1;
-    dims.push_back({L.dim, L.stride, L.box});
-  }
-  if (dims.size() > 5) return false;
-  for (auto& dm : dims) if (dm.box > 256 || dm.ext >= (1LL << 31)) return false;
-  if (dims[0].box < 2) return false;
-  // staging offsets (box order, dims[0] innermost)
-  int64_t bstride[5] = {1, 1, 1, 1, 1};
-  for (size_t k = 1; k < dims.size(); ++k) bstride[k] = bstride[k - 1] * dims[k - 1].box;
-  for (int r = 0; r < 32; ++r) {
-    int64_t rr = r, off = 0;
-    for (int j = d.nf - 1; j >= 0; --j) {
-      const Leg& L = legs[j];
-      if (L.box <= 1) continue;
-      off += (rr % L.box) * L.mult * bstride[L.tdim];
-      rr /= L.box;
-    }
-    p.o_roff[r] = (int16_t)off;
-  }
-  for (int c = 0; c < 16; ++c) {
-    int64_t cc = c, off = 0;
-    for (int i = d.nn - 1; i >= 0; --i) {
-      const Leg& L = legs[d.nf + i];
-      if (L.box <= 1) continue;
-      off += (cc % L.box) * L.mult * bstride[L.tdim];
-      cc /= L.box;
-    }
-    p.o_coff[c] = (int16_t)off;
-  }
-  for (int j = 0; j < d.nf; ++j) { p.f_tdim[j] = (int8_t)legs[j].tdim; p.f_tmul[j] = (int32_t)legs[j].mult; }
-  for (int i = 0; i < d.nn; ++i) {
-    p.n_tdim[i] = (int8_t)legs[d.nf + i].tdim; p.n_tmul[i] = (int32_t)legs[d.nf + i].mult; p.n_dim[i] = d.n_dim[i];
-  }
-  p.nn = d.nn;
-  p.z_tdim = legs.back().tdim;
-  p.z_tmul = (int32_t)legs.back().mult;
-  // 128B swizzle when the inner box is one 128-byte run of result columns
-  // (lanes = rows then write distinct 16-byte chunks: conflict-free staging)
-  bool inner_cols = true;
-  for (int li : ord) if (legs[li].tdim == 0 && legs[li].kind != 1 && legs[li].dim > 1) inner_cols = false;
-  p.o_swz = (inner_cols && dims[0].box == 16) ? 1 : 0;
-  cuuint64_t gdim[5], gstr[4];
-  cuuint32_t box[5], estr[5];
-  for (size_t k = 0; k < dims.size(); ++k) {
-    gdim[k] = (cuuint64_t)dims[k].ext;
-    box[k] = (cuuint32_t)dims[k].box;
-    estr[k] = 1;
-    if (k) gstr[k - 1] = (cuuint64_t)(dims[k].stride * 8);
-  }
-  if (enc(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, (cuuint32_t)dims.size(), d.out, gdim, gstr, box, estr,
-          CU_TENSOR_MAP_INTERLEAVE_NONE, p.o_swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
-          CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return false;
-  p.o_rank = (int32_t)dims.size();
-  p.tma_out = 1;
-  return true;
-}
-
-// TNC_TC16=0 keeps complex64 GEMM steps on 3xTF32 even when amax_in is given
-inline bool tc16_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("TNC_TC16");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v != 0;
-}
+// complex64 GEMM steps with an input bound (amax_in) run on fp16-split operands
+inline bool tc16_enabled() { return true; }
 
 // engine step on the GEMM path; returns 1 launched, 0 not applicable, -1 error
 // (when launched with amax_out set, the epilogue has recorded max |out| per z)
@@ -927,14 +779,16 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
       p.NT = 128;
       p.tiles_n = (int)((d.N + p.NT - 1) / p.NT);
     }
-    if (const char* e = getenv("TNC_TG_NT")) {
-      const int nt = atoi(e);
-      if (nt >= 16 && nt % 16 == 0 && nt <= (f16 ? 128 : 64) && d.N >= nt) {
-        p.NT = nt;
-        p.tiles_n = (int)((d.N + p.NT - 1) / p.NT);
-      }
+    // same decisions as the kernel: A-resident 4M tiles for K <= 128 with
+    // several column tiles, 3M (Gauss) products on the other 128-wide F16 tiles
+    bool ares = false;
+    {
+      const bool alt = f16 && p.NT <= 32;
+      const int TS = alt ? 4 : (p.NT > 64 ? 1 : 2);
+      const int acols = f16 ? 2 * KC : 4 * KC;
+      ares = f16 && p.tiles_n > 1 && TS * 2 * p.NT + p.nchunk * acols <= 512 && p.nchunk <= TC_MAX_STAGES;
     }
-    if (const char* e = getenv("TNC_TG_DEBUG")) p.dbg = atoi(e);
+    p.g3 = (f16 && p.NT == 128 && !ares) ? 1 : 0;
     // stages: fill the shared-memory budget
     int RS = 4, BS = 3;
     const size_t budget = 226 * 1024;
@@ -950,13 +804,9 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
         p.blk_contig = 1;
     }
     const int64_t cn = p.cn_smem ? d.N : 0;
-    CUtensorMap tmO;
-    const int tma = tg_out_map(d, p, tmO, enc) ? 1 : 0;
-    while (RS + 1 <= TG_MAX_RS && tg_smem_bytes(p.NT, KC, RS + 1, BS, f16, cn, tma) <= budget) ++RS;
-    while (BS + 1 <= TG_MAX_BS && tg_smem_bytes(p.NT, KC, RS, BS + 1, f16, cn, tma) <= budget) ++BS;
-    if (const char* e = getenv("TNC_TG_RS")) RS = atoi(e);
-    if (const char* e = getenv("TNC_TG_BS")) BS = atoi(e);
-    if (tg_smem_bytes(p.NT, KC, RS, BS, f16, cn, tma) > budget) return 0;
+    while (RS + 1 <= TG_MAX_RS && tg_smem_bytes(p.NT, KC, RS + 1, BS, f16, cn) <= budget) ++RS;
+    while (BS + 1 <= TG_MAX_BS && tg_smem_bytes(p.NT, KC, RS, BS + 1, f16, cn) <= budget) ++BS;
+    if (tg_smem_bytes(p.NT, KC, RS, BS, f16, cn) > budget) return 0;
     p.RS = RS; p.BS = BS;
     // A: [Z][M][2K floats] with row pitch K complex, batch pitch acc_zstride complex
     CUtensorMap tm;
@@ -994,22 +844,25 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     p.items = p.Z * p.tiles_m * p.tiles_n;
     p.per_cta = (p.items + sms - 1) / sms;
-    p.ilv = 0;                     // round-robin tiles (TNC_TG_ILV=1) measured neutral
-    if (const char* e = getenv("TNC_TG_ILV")) p.ilv = atoi(e);
-    const int64_t grid = p.ilv ? std::min<int64_t>(sms, p.Z * p.tiles_m) : (p.items + p.per_cta - 1) / p.per_cta;
-    const size_t smem = tg_smem_bytes(p.NT, KC, RS, BS, f16, cn, tma);
+    // A-resident tiles keep each row tile on one CTA (contiguous items);
+    // otherwise items go round-robin so a row tile's column tiles run on
+    // neighbouring CTAs together and share the A tile through L2
+    p.ilv = (ares || p.tiles_n == 1) ? 0 : 2;
+    const int64_t grid = p.ilv == 2 ? std::min<int64_t>(sms, p.items) : (p.items + p.per_cta - 1) / p.per_cta;
+    const size_t smem = tg_smem_bytes(p.NT, KC, RS, BS, f16, cn);
     static uint64_t attr = 0;
     int adev = 0;
     if (attr_needed(attr, &adev)) {
       cudaFuncSetAttribute(k_tc_gemm<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       cudaFuncSetAttribute(k_tc_gemm<16, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       cudaFuncSetAttribute(k_tc_gemm<16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      cudaFuncSetAttribute(k_tc_gemm<16, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       attr |= 1ull << (adev & 63);
     }
-    const CUtensorMap& to = tma ? tmO : tm;
-    if (f16) k_tc_gemm<16, true><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm, to);
-    else if (KC == 16) k_tc_gemm<16, false><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm, to);
-    else k_tc_gemm<8, false><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm, to);
+    if (p.g3) k_tc_gemm<16, true, true><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm);
+    else if (f16) k_tc_gemm<16, true><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm);
+    else if (KC == 16) k_tc_gemm<16, false><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm);
+    else k_tc_gemm<8, false><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm);
     const bool ok = cudaGetLastError() == cudaSuccess;
     cudaFreeAsync(bp, s);
     return ok ? 1 : -1;

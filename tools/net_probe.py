@@ -65,6 +65,9 @@ def main():
     ap.add_argument("--z", type=int, default=0, help="max batch elements per device pass (0: auto)")
     ap.add_argument("--full", action="store_true")
     ap.add_argument("--json", default=None)
+    ap.add_argument("--ncu-step", type=int, default=-1,
+                    help="after the timing, relaunch this step alone between cudaProfilerStart/Stop "
+                         "(ncu --profile-from-start off captures just it)")
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     t0 = time.perf_counter()
@@ -112,6 +115,11 @@ def main():
         NV.check(L.tnc_step(C.byref(ex._steps[i]), sptr), "tnc_step")
         evs[i + 1].record(stream)
     torch.cuda.synchronize()
+    if args.ncu_step >= 0:
+        torch.cuda.profiler.start()
+        NV.check(L.tnc_step(C.byref(ex._steps[args.ncu_step]), sptr), "tnc_step")
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
     peaks = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                         "MEASURED_PEAKS.json")))
     hbm, bf16 = peaks["hbm_gbs"], peaks["bf16_tflops"]
