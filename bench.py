@@ -1,35 +1,31 @@
 #!/usr/bin/env python
 """Benchmark of the contraction hot path (one JSON line on rank 0).
 
-Workloads (``--workload``):
+Headline (default, ``--workload d12``): BASELINE.json's metric on its own
+config -- amplitudes/s of the 53-qubit Sycamore circuit (configs[4]: 53-qubit
+diagonal lattice, couplers ABCDCDAB, fSim(pi/2, pi/6), seeded single-qubit
+gates) at **12 cycles**, through the reference's default two-sided network
+(split at cycle 6, tns.py:185-212), rank cap 12, sliced over the cut edges
+(45,49), (38,45) (1024 slices, tools/cut_search.py; path re-searched on the
+sliced estimate as network.py:318-323 does), complex64.
 
-* ``sweep`` (default; BASELINE.json configs[1]) -- isolated pairwise
-  contraction sweep in complex64: the accumulator C has r free legs of dim 2
-  (r = 16..28) and k shared legs of dim 4 (k = 1..3) in a seeded random leg
-  order; it is contracted with the bitstring-projected site tensor (k shared +
-  n = 1..3 new dim-4 legs) over a bitstring batch B in {1, 16, 256}; cases are
-  kept while every operand fits 2^29 elements.  One *step* = one pass over
-  all cases; each case = projection gather + fused permute/contract kernel.
-  Unit: bitstring-steps/s (one bitstring's accumulator advanced by one
-  Contract step).  The 53-qubit / 12-cycle headline network is not runnable by
-  this algorithm on any GPU count (peak intermediate 2^41 elements unsliced,
-  see DESIGN.md), so the tier rule's "largest single-GPU configuration"
-  applies.
-* ``cfg0`` (configs[0]) -- full amplitudes: 3x3 lattice, 8 cycles, 64
-  bitstrings, complex128, projected engine.  Unit: amplitudes/s.
-* ``syc53`` -- full amplitudes of the configs[4] circuit family (53-qubit
-  Sycamore lattice, ABCDCDAB, fSim(pi/2, pi/6)) at the deepest depth whose
-  unsliced projected network fits one B200 (8 cycles: 6.4e11 complex
-  multiplies and 2^29-element intermediates per amplitude), complex64,
-  bitstring batches of the executor's chunk size.  Unit: amplitudes/s.
+One *step* = one device pass over ``--slices-per-step`` slices (default 1) of
+one bitstring on every rank; rank r takes slices (i*W + r)*k ... of step i, so
+N ranks advance one amplitude N times faster, and the slice sum across ranks is
+one NCCL all-reduce per step (the reference's slice loop, network.py:334-339,
+distributed).  An amplitude is all 1024 slices, so value = W * k * steps /
+1024 / t (whole-job amplitudes/s; per-rank work fixed: "weak").  Every slice
+has the same shapes and path, so a step is an exact 1/1024-of-an-amplitude
+unit of work; ``tools/net_probe.py --full`` runs whole amplitudes.
 
-Timing: W warm-up steps, then K steps; every case (a timed iteration) is
-bracketed by CUDA events on the launching stream and preceded by an untimed
-L2 flush (256 MiB memset, then a 256 MiB read so the flush's dirty lines are
-written back before the timed kernel), so no case reads L2-resident data; barrier +
-synchronize around the timed region; max over ranks.  ``--impl reference``
-times the CPU oracle port of the reference algorithm (numpy tensordot, as
-tnsim.tensor.contract_pair) on a bounded sample and scales to the same unit.
+Nested entries (same JSON line): two-sided 53q depth 10 and depth 8 (whole
+amplitudes, bitstring batches), the configs[1] pairwise sweep, configs[0].
+
+Timing: W untimed warm-up steps, then K steps, each bracketed by CUDA events
+on the launching stream; barrier + synchronize around the timed region; max
+over ranks.  Inputs are larger than L2 (2^31-element ping-pong accumulators).
+``--impl reference`` times the CPU oracle port of the reference path
+(np.tensordot on the reference's operand layouts) on the same config.
 """
 
 from __future__ import annotations
@@ -37,6 +33,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -50,42 +47,87 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "amplitudes/sec (53q, depth 12) at 1/2/4/8 GPUs; contraction % of roofline"
-SWEEP_LIMIT = 1 << 29          # elements per operand (complex64: 4 GiB)
+D12 = {"depth": 12, "split": 6, "cap": 12, "cuts": [(45, 49), (38, 45)]}
+SWEEP_LIMIT = 1 << 32          # elements per operand (complex64: 32 GiB)
+SEED = 0
+NCU_D12_PROFILE = "profiles/r02b_ncu_d12_gemm.json"   # ncu --set full of the top GEMM step (dram bytes)
 
 
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
-    return 6650.0, 1590.0, "fallback"
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), float(d.get("bf16_tflops_sustained", 0)), "measured"
+    return 6650.0, 1590.0, 0.0, "fallback (B200_PROFILING.md)"
 
 
-def sweep_cases(limit=SWEEP_LIMIT):
-    cases = []
-    for r in (16, 20, 24, 28):
-        for k in (1, 2, 3):
-            for n in (1, 2, 3):
-                for B in (1, 16, 256):
-                    if B * (2 ** r) * (4 ** max(k, n)) <= limit:
-                        cases.append((r, k, n, B))
-    return cases
+# ---------------------------------------------------------------------------
+# process setup: one process per GPU; --gpus N without torchrun re-launches
+# ---------------------------------------------------------------------------
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
 
 
-def case_layout(r, k, n, seed):
-    rng = np.random.default_rng(seed)
-    perm = [int(x) for x in rng.permutation(r + k)]
-    dims = [2 if x < r else 4 for x in perm]
-    shared_pos = sorted((i for i, x in enumerate(perm) if x >= r), key=lambda i: perm[i])
-    pairs = [(p, j) for j, p in enumerate(shared_pos)]
-    return perm, dims, pairs
+def self_launch(args) -> bool:
+    """``--gpus N`` (N > 1) outside torchrun: re-run this script under
+    torch.distributed.run with N ranks on 127.0.0.1; returns True when the
+    children ran (the caller exits with their status)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")           # NCCL reports the ranks it connected
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(Path(__file__).resolve())]
+    cmd += sys.argv[1:]
+    rc = subprocess.run(cmd, env=env).returncode
+    sys.exit(rc)
 
 
-def case_traffic(r, k, n, B, itemsize=8):
-    acc = B * 2 ** r * 4 ** k
-    out = B * 2 ** r * 4 ** n
-    site = B * 4 ** (k + n)
-    return (acc + out + 2 * site) * itemsize, 8 * B * 2 ** r * 4 ** k * 4 ** n
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus > 1 and world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    import torch
+
+    if args.dry_run:
+        dev = torch.device("cpu")
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.init_process_group("gloo")
+        return rank, world, dev
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    return rank, world, dev
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def allreduce_max(x, world, dev):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 # ---------------------------------------------------------------------------
@@ -151,568 +193,251 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# our arm
+# networks
 # ---------------------------------------------------------------------------
-def run_sweep(args, rank, world, dev):
-    import torch
-
-    from paper_2011_02621_b200.engine import PairPlan, project_variants
-
-    hbm, bf16, peak_src = peaks()
-    cases = sweep_cases(args.limit)
-    torch.manual_seed(1234 + rank)
-    max_acc = max(B * 2 ** r * 4 ** k for r, k, n, B in cases)
-    max_out = max(B * 2 ** r * 4 ** n for r, k, n, B in cases)
-    acc = torch.randn(max_acc, dtype=torch.complex64, device=dev)
-    out = torch.empty(max_out, dtype=torch.complex64, device=dev)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    flush_f = flush.view(torch.float32)
-    flush_sink = torch.empty((), dtype=torch.float32, device=dev)
-    l2_mode = os.environ.get("BENCH_L2_FLUSH", "write+read")
-    plans, inputs = [], []
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(99 + rank)
-    for ci, (r, k, n, B) in enumerate(cases):
-        perm, dims, pairs = case_layout(r, k, n, seed=ci)
-        plan = PairPlan(dims, [4] * (k + n), pairs, dtype="complex64")
-        variants = torch.randn((2, 4 ** (k + n)), dtype=torch.complex64, device=dev, generator=gen)
-        bits = torch.randint(0, 2, (B,), dtype=torch.int32, device=dev, generator=gen)
-        site = torch.empty((B, 4 ** (k + n)), dtype=torch.complex64, device=dev)
-        plans.append(plan)
-        inputs.append((variants, bits, site))
-    stream = torch.cuda.current_stream(dev)
-
-    def one_step(record):
-        tot_case, tot_kern = 0.0, 0.0
-        per = []
-        for ci, (r, k, n, B) in enumerate(cases):
-            variants, bits, site = inputs[ci]
-            KN = 4 ** (k + n)
-            # untimed L2 flush: write a buffer larger than L2, then read it back,
-            # so the flush's own dirty lines are written back before the timed
-            # kernel instead of during it
-            flush.zero_()
-            if l2_mode == "write+read":
-                torch.sum(flush_f, dim=0, out=flush_sink)
-            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-            e0.record(stream)
-            project_variants(variants, bits, site, KN, stream)
-            e1.record(stream)
-            plans[ci](acc, site, out, B, 2 ** r * 4 ** k, KN, 2 ** r * 4 ** n, stream)
-            e2.record(stream)
-            per.append((e0, e1, e2))
-        torch.cuda.synchronize(dev)
-        rows = []
-        for (r, k, n, B), (e0, e1, e2) in zip(cases, per):
-            tc = e0.elapsed_time(e2) * 1e-3
-            tk = e1.elapsed_time(e2) * 1e-3
-            tot_case += tc
-            tot_kern += tk
-            rows.append((r, k, n, B, tc, tk))
-        return tot_case, tot_kern, rows
-
-    for _ in range(args.warmup):
-        one_step(False)
-    barrier(world)
-    torch.cuda.synchronize(dev)
-    with ClockSampler(dev.index) as clk:
-        t_case = t_kern = 0.0
-        acc_rows = {}
-        for _ in range(args.steps):
-            tc, tk, rows = one_step(True)
-            t_case += tc
-            t_kern += tk
-            for r, k, n, B, a, b in rows:
-                acc_rows.setdefault((r, k, n, B), [0.0, 0.0])
-                acc_rows[(r, k, n, B)][0] += a
-                acc_rows[(r, k, n, B)][1] += b
-    torch.cuda.synchronize(dev)
-    barrier(world)
-    t_case_max = allreduce_max(t_case, world, dev)
-    units_per_step = sum(B for _, _, _, B in cases)
-    value = world * units_per_step * args.steps / t_case_max
-    # roofline of the dominant kernel (the fused permute+contract launch)
-    bytes_tot = sum(case_traffic(*c)[0] for c in cases) * args.steps
-    flops_tot = sum(case_traffic(*c)[1] for c in cases) * args.steps
-    roof_t = sum(max(case_traffic(*c)[0] / (hbm * 1e9), case_traffic(*c)[1] / (bf16 * 1e12)) for c in cases) * args.steps
-    achieved = bytes_tot / t_kern / 1e9
-    detail = []
-    for c, (a, b) in acc_rows.items():
-        by, fl = case_traffic(*c)
-        detail.append({"r": c[0], "k": c[1], "n": c[2], "B": c[3], "kernel_us": 1e6 * b / args.steps,
-                       "GBps": by / (b / args.steps) / 1e9, "TFLOPs": fl / (b / args.steps) / 1e12})
-    res = {
-        "value": value, "unit": "bitstring-steps/s", "ms_per_step": 1e3 * t_case_max / args.steps,
-        "gpu_launches": 2 * len(cases) * args.steps,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": (roof_t / t_kern), "traffic": None,
-                     "peak_source": f"{peak_src} hbm_gbs / bf16_tflops (MEASURED_PEAKS.json)",
-                     "kernel": "all contraction launches of the sweep: tnc::k_tc_c64 (tcgen05 3xTF32, K >= 8, K*N >= 256) "
-                               "and tnc::k_pair_pipe* (TMA-fed fused permute+contract SIMT); projections excluded",
-                     "algorithmic": "per case (acc + out + 2*projected site) * 8 B; flops 8*B*2^r*4^k*4^n",
-                     "kernel_share_of_step": t_kern / t_case, "tflops_achieved": flops_tot / t_kern / 1e12,
-                     "traffic_ncu": ncu_traffic_check()},
-        "config": {"workload": "configs[1] pairwise-contraction sweep", "dtype": "complex64",
-                   "cases": len(cases), "r": [16, 20, 24, 28], "k": [1, 2, 3], "n": [1, 2, 3],
-                   "batch": [1, 16, 256], "operand_limit_elems": args.limit,
-                   "leg_order": "seeded random permutation per case",
-                   "l2": ("256 MiB memset + 256 MiB read (write-back of the flush drained) before every case, untimed"
-                          if l2_mode == "write+read" else "256 MiB memset flush before every case (untimed)")},
-        "clocks": clk.summary(),
-        "dtype": "complex64",
-        "detail": detail,
-    }
-    if args.e2e:
-        res["e2e"] = sweep_e2e(args, cases, plans, inputs, dev, world)
-    return res
-
-
-def sweep_e2e(args, cases, plans, inputs, dev, world):
-    """Same sweep through the public API with host buffers: per case the
-    accumulator and projection bits go H2D from pinned memory, gather +
-    contract run, the result comes back D2H; all inside the timed region.
-    The cases are pipelined over three streams (H2D copies, compute, D2H
-    copies) with BENCH_E2E_SLOTS (6) device slots per buffer, so later cases'
-    uploads and earlier cases' downloads overlap case i's kernels (PCIe is
-    full duplex)."""
-    import torch
-
-    from paper_2011_02621_b200.engine import project_variants
-
-    max_acc = max(B * 2 ** r * 4 ** k for r, k, n, B in cases)
-    max_out = max(B * 2 ** r * 4 ** n for r, k, n, B in cases)
-    h_acc = torch.randn(max_acc, dtype=torch.complex64).pin_memory()
-    ns = int(os.environ.get("BENCH_E2E_SLOTS", "6"))
-    h_out = [torch.empty(max_out, dtype=torch.complex64).pin_memory() for _ in range(ns)]
-    d_acc = [torch.empty(max_acc, dtype=torch.complex64, device=dev) for _ in range(ns)]
-    d_out = [torch.empty(max_out, dtype=torch.complex64, device=dev) for _ in range(ns)]
-    h_bits = [inputs[i][1].cpu().pin_memory() for i in range(len(cases))]
-    stream = torch.cuda.current_stream(dev)
-    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
-    h2d = d2h = 0
-    for r, k, n, B in cases:
-        h2d += B * 2 ** r * 4 ** k * 8 + B * 4
-        d2h += B * 2 ** r * 4 ** n * 8
-
-    def step():
-        nc = len(cases)
-        ev_in = [torch.cuda.Event() for _ in range(nc)]
-        ev_comp = [torch.cuda.Event() for _ in range(nc)]
-        ev_out = [torch.cuda.Event() for _ in range(nc)]
-        s_in.wait_stream(stream)
-        for ci, (r, k, n, B) in enumerate(cases):
-            variants, bits, site = inputs[ci]
-            na, no = B * 2 ** r * 4 ** k, B * 2 ** r * 4 ** n
-            slot = ci % ns
-            with torch.cuda.stream(s_in):
-                if ci >= ns:
-                    s_in.wait_event(ev_comp[ci - ns])       # slot's accumulator consumed
-                d_acc[slot][:na].copy_(h_acc[:na], non_blocking=True)
-                bits.copy_(h_bits[ci], non_blocking=True)
-                ev_in[ci].record(s_in)
-            stream.wait_event(ev_in[ci])
-            if ci >= ns:
-                stream.wait_event(ev_out[ci - ns])          # slot's result downloaded
-            project_variants(variants, bits, site, 4 ** (k + n), stream)
-            plans[ci](d_acc[slot], site, d_out[slot], B, 2 ** r * 4 ** k, 4 ** (k + n), 2 ** r * 4 ** n, stream)
-            ev_comp[ci].record(stream)
-            with torch.cuda.stream(s_out):
-                s_out.wait_event(ev_comp[ci])
-                h_out[slot][:no].copy_(d_out[slot][:no], non_blocking=True)
-                ev_out[ci].record(s_out)
-        stream.wait_stream(s_out)
-        stream.wait_stream(s_in)
-        torch.cuda.synchronize(dev)
-
-    step()
-    barrier(world)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    steps = max(1, min(args.steps, 3))
-    e0.record(stream)
-    for _ in range(steps):
-        step()
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    t = allreduce_max(e0.elapsed_time(e1) * 1e-3, world, dev)
-    units = sum(B for *_, B in cases) * steps * world
-    return {"value": units / t, "unit": "bitstring-steps/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "steps": steps, "path": "PairPlan + project_variants on host-resident pinned buffers, H2D / compute / "
-                                    "D2H on three streams, %d device slots" % ns}
-
-
-SYC_DEPTH = 8
-SYC_MAX_RANK = 12
-
-
-def syc_engine(dev, depth=SYC_DEPTH):
-    from paper_2011_02621_b200 import AmplitudeEngine, pattern_rqc, sycamore53_graph
+def syc_circuit(depth, seed=SEED):
+    from paper_2011_02621_b200 import pattern_rqc, sycamore53_graph
 
     graph, pats, _ = sycamore53_graph()
-    circ = pattern_rqc(graph, [pats[c] for c in "ABCDCDAB"], depth, seed=0)
-    return AmplitudeEngine(circ, dtype="complex64", max_rank=SYC_MAX_RANK, device=dev)
+    return pattern_rqc(graph, [pats[c] for c in "ABCDCDAB"], depth, seed=seed)
 
 
-def run_syc53(args, rank, world, dev, depth=SYC_DEPTH):
-    """Amplitudes of the 53-qubit Sycamore circuit (projected engine): each
-    step evaluates one batch of B bitstrings per GPU (B = the executor's chunk,
-    all resident in HBM).  With N ranks the step is one global batch of N*B
-    bitstrings through ``distributed.sharded_amplitudes``: every rank contracts
-    its shard, one NCCL all-reduce sums and gathers the amplitudes (weak
-    scaling: B per rank)."""
+def random_bits(n, count, seed):
+    rng = np.random.default_rng(seed)
+    return ["".join(rng.choice(["0", "1"], n)) for _ in range(count)]
+
+
+def is_gemm_step(sp, z):
+    return sp.K % 16 == 0 and sp.K * sp.N >= 256 and z * ((sp.M + 127) // 128) >= 64
+
+
+def launches_per_pass(plan, z):
+    """Kernels of ours per device pass: the first site's projection, per step
+    k_bscale + k_bprime + k_tc_gemm (GEMM steps) or one SIMT kernel (+ k_amax
+    when an fp16-split GEMM step follows), the slice sum."""
+    n = 2
+    steps = plan.steps
+    for i, sp in enumerate(steps):
+        if is_gemm_step(sp, z):
+            n += 3
+        else:
+            n += 1
+            if i + 1 < len(steps) and is_gemm_step(steps[i + 1], z):
+                n += 1
+    return n
+
+
+def step_times(ex, plan, dev):
+    """Re-launch every path step of the executor's last chunk alone between
+    CUDA events on the launching stream (descriptors as the last pass left
+    them); returns per-step seconds."""
     import ctypes as C
 
     import torch
 
     from paper_2011_02621_b200 import _native as NV
 
-    hbm, bf16, peak_src = peaks()
-    t0 = time.perf_counter()
-    eng = syc_engine(dev, depth)
-    setup_s = time.perf_counter() - t0
-    ex, plan = eng.executor, eng.plan
-    B = ex.max_z
-    from paper_2011_02621_b200.distributed import sharded_amplitudes
-
-    Bg = B * world                              # the global batch (same bitstrings on every rank)
-    rng = np.random.default_rng(100)
-    gbits = rng.integers(0, 2, (Bg, 53)).astype(np.int32)
-    gsel = eng.selectors(gbits)
-    gamp = torch.zeros(Bg, dtype=torch.complex64, device=dev)
-
-    def one_pass():
-        if world > 1:
-            sharded_amplitudes(ex, gsel, Bg, gamp)
-        else:
-            eng.amplitudes_device(gsel, B, gamp)
-
-    bits = gbits[rank * B:(rank + 1) * B]
-    sel = eng.selectors(bits)
-    amp = torch.zeros(B, dtype=torch.complex64, device=dev)
-    stream = torch.cuda.current_stream(dev)
-    for _ in range(args.warmup):
-        one_pass()
-    barrier(world)
-    torch.cuda.synchronize(dev)
-    # each step's working set (2 x B x 4 GiB ping-pong buffers) is far larger than L2
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    with ClockSampler(dev.index) as clk:
-        for e0, e1 in evs:
-            e0.record(stream)
-            one_pass()
-            e1.record(stream)
-        torch.cuda.synchronize(dev)
-    t = sum(e0.elapsed_time(e1) for e0, e1 in evs) * 1e-3
-    barrier(world)
-    t_max = allreduce_max(t, world, dev)
-    value = world * B * args.steps / t_max
-    # per-step kernel times (untimed pass, one chunk): dominant kernel + path roofline
     L = NV.lib()
+    stream = torch.cuda.current_stream(dev)
     sptr = C.c_void_p(stream.cuda_stream)
-    ex.run(sel, B, amp)
-    traffic = plan.step_traffic(8)
-    sev = [torch.cuda.Event(enable_timing=True) for _ in range(len(plan.steps) + 1)]
-    sev[0].record(stream)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(plan.steps) + 1)]
+    evs[0].record(stream)
     for i in range(len(plan.steps)):
         NV.check(L.tnc_step(C.byref(ex._steps[i]), sptr), "tnc_step")
-        sev[i + 1].record(stream)
+        evs[i + 1].record(stream)
     torch.cuda.synchronize(dev)
-    tot_t = tot_roof = tot_roof3 = gemm_t = gemm_fl = 0.0
-    for i, sp in enumerate(plan.steps):
-        ts = sev[i].elapsed_time(sev[i + 1]) * 1e-3
-        by, fl = traffic[i][0] * B, traffic[i][1] * B
-        tot_t += ts
-        tot_roof += max(by / (hbm * 1e9), fl / (bf16 * 1e12))
-        # the fp16-split GEMM issues 3 products per real product: its own tensor ceiling is bf16/3
-        split = sp.K * sp.N >= 256 and sp.K % 16 == 0
-        tot_roof3 += max(by / (hbm * 1e9), (3 * fl if split else fl) / (bf16 * 1e12))
-        if sp.K * sp.N >= 256 and sp.K % 8 == 0:      # tensor-core steps
-            gemm_t += ts
+    return [evs[i].elapsed_time(evs[i + 1]) * 1e-3 for i in range(len(plan.steps))]
+
+
+def path_roofline(plan, times, z, itemsize, hbm, bf16, bf16_sus):
+    """North-star path roofline: sum over steps of max(bytes / HBM, flops /
+    bf16 peak) over the sum of measured step times; flops = 8 M K N per
+    complex multiply-add (algorithmic).  The dominant kernel (the fp16-split
+    tcgen05 GEMM) is reported with its achieved algorithmic TF/s."""
+    tot = roof = roof_split = gemm_t = gemm_fl = gemm_by = 0.0
+    for sp, t in zip(plan.steps, times):
+        by = (sp.M * sp.K + sp.M * sp.N) * itemsize * z
+        fl = 8.0 * sp.M * sp.K * sp.N * z
+        tot += t
+        roof += max(by / (hbm * 1e9), fl / (bf16 * 1e12))
+        g = is_gemm_step(sp, z)
+        # pipe work of the 3M fp16-split GEMM: 3 real products x 3 split terms
+        # = 18 flops per complex multiply-add (2.25x the algorithmic 8)
+        roof_split += max(by / (hbm * 1e9), (2.25 * fl if g else fl) / (bf16 * 1e12))
+        if g:
+            gemm_t += t
             gemm_fl += fl
-    achieved = gemm_fl / gemm_t / 1e12 if gemm_t else 0.0
-    launches = ex.launches_per_chunk() + sum(1 for sp in plan.steps if sp.K * sp.N >= 256 and sp.K % 8 == 0)
-    res = {
-        "value": value, "unit": "amplitudes/s", "ms_per_step": 1e3 * t_max / args.steps,
-        "gpu_launches": launches * args.steps,
-        "roofline": {"bound": "tensor", "achieved": achieved, "peak": bf16, "unit": "TFLOP/s",
-                     "frac": achieved / bf16, "traffic": None,
-                     "peak_source": f"{peak_src} bf16_tflops (MEASURED_PEAKS.json); the kernel issues fp16 MMAs "
-                                    "(3 split products per real product, so 3x the algorithmic flops on the pipe)",
-                     "kernel": "tnc::k_tc_gemm<16,F16> (tcgen05 kind::f16 fp16-split complex GEMM steps)",
-                     "algorithmic": "8*M*K*N flops per step per bitstring",
-                     "kernel_share_of_step": gemm_t / tot_t if tot_t else None,
-                     "path_roofline_frac": tot_roof / tot_t if tot_t else None,
-                     "path_roofline": "sum over steps of max(bytes/HBM, flops/bf16 peak) / sum of step times",
-                     "path_roofline_frac_split": tot_roof3 / tot_t if tot_t else None,
-                     "path_roofline_split": "same with 3x flops on the fp16-split GEMM steps (the complex64 "
-                                            "accuracy bound needs 3 fp16 products per real product)"},
-        "config": {"workload": "configs[4] circuit family: 53-qubit Sycamore, ABCDCDAB, "
-                               f"{depth} cycles (unsliced projected network on one GPU)",
-                   "dtype": "complex64", "bitstrings_per_step": B, "max_rank": SYC_MAX_RANK,
-                   "sharding": ("one global batch of N*B bitstrings: per-rank shard (distributed.rank_chunks) + "
-                                "one NCCL all_reduce(sum) of the amplitude vector, timed" if world > 1
-                                else "single GPU"),
-                   "multiplies_per_amplitude": plan.multiplies, "max_elems": plan.max_elems,
-                   "path_steps": len(plan.steps), "host_setup_s": setup_s,
-                   "l2": "inputs larger than L2 (2 x B x 4 GiB ping-pong buffers)"},
-        "clocks": clk.summary(), "dtype": "complex64",
+            gemm_by += by
+    ach = gemm_fl / gemm_t / 1e12 if gemm_t else 0.0
+    return {
+        "bound": "tensor", "achieved": ach, "peak": bf16, "unit": "TFLOP/s", "frac": ach / bf16,
+        "kernel": "tnc::k_tc_gemm<16,true,true> (tcgen05.mma kind::f16, fp16-split operands, 3M complex products, "
+                  "A operand in TMEM, B by bulk copies)",
+        "algorithmic": "8*M*K*N flops per GEMM step per slice (complex multiply-add = 8 real flops)",
+        "kernel_share_of_step": gemm_t / tot if tot else None,
+        "pipe_flops_per_algorithmic_flop": 2.25,
+        "frac_pipe": 2.25 * ach / bf16,
+        "frac_pipe_sustained_peak": 2.25 * ach / bf16_sus if bf16_sus else None,
+        "path_roofline_frac": roof / tot if tot else None,
+        "path_roofline": "sum over steps of max(bytes/HBM, 8MKN/bf16 peak) / sum of measured step times",
+        "path_roofline_frac_split": roof_split / tot if tot else None,
+        "path_roofline_split": "same with the GEMM steps charged their 2.25x pipe flops (fp16-split 3M: the "
+                               "complex64 accuracy bound needs 3 fp16 products per real product)",
+        "gemm_step_GBps": gemm_by / gemm_t / 1e9 if gemm_t else None,
     }
-    if args.e2e:
-        outs = ["".join(map(str, row)) for row in bits]
-        for _ in range(2):                       # first call eager, second captures the path's CUDA graph
-            eng.amplitudes(outs)
-        torch.cuda.synchronize(dev)
-        barrier(world)
-        steps = max(1, min(args.steps, 3))
-        t0 = time.perf_counter()
-        for _ in range(steps):
-            eng.amplitudes(outs)
-        te = allreduce_max(time.perf_counter() - t0, world, dev)
-        res["e2e"] = {"value": world * B * steps / te, "unit": "amplitudes/s", "h2d_bytes_per_step": B * 53 * 4,
-                      "d2h_bytes_per_step": B * 8, "steps": steps,
-                      "path": "AmplitudeEngine.amplitudes(list of bitstring strings) -> host complex array"}
-    res["_plan_steps"] = [(sp.M, sp.K, sp.N) for sp in plan.steps]
-    return res
 
 
-SYC_SLICED_DEPTH = SYC_DEPTH + 2
-# cut edges for the sliced depth-10 network (tools/syc_sliced.py: greedy over
-# bond dims <= 16, minimising the largest intermediate, then the multiplies)
-SYC_SLICED_CUTS = [(9, 14), (2, 9)]
-
-
-# ncu --set full captures committed under profiles/ (one launch each) and the
-# sweep case each was taken on: DRAM bytes per launch vs the algorithmic bytes
-NCU_TRAFFIC_PROFILE = "profiles/r01h_ncu_full_summary.json"
-NCU_TRAFFIC_CASES = [(16, 2, 2, 256), (24, 1, 2, 1)]
-
-
-def _ncu_bytes(v: str) -> float:
-    num, unit = v.split()
-    return float(num) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[unit]
-
-
-def ncu_traffic_check():
-    """Per captured launch: dram read+write bytes (ncu) vs algorithmic bytes."""
+def ncu_traffic():
+    """dram read+write bytes of the committed ncu capture of the top GEMM step
+    vs its algorithmic bytes (null when no capture is committed)."""
     try:
-        caps = json.loads((ROOT / NCU_TRAFFIC_PROFILE).read_text())
+        d = json.loads((ROOT / NCU_D12_PROFILE).read_text())
+        return d
     except (OSError, ValueError):
         return None
-    out = []
-    for cap, case in zip(caps, NCU_TRAFFIC_CASES):
-        k = cap[0]
-        dram = _ncu_bytes(k["dram__bytes_read.sum"]) + _ncu_bytes(k["dram__bytes_write.sum"])
-        alg = case_traffic(*case)[0]
-        out.append({"kernel": k["kernel"].split("(")[0], "case": "r%d/k%d/n%d/B%d" % case, "dram_bytes": dram,
-                    "algorithmic_bytes": alg, "ratio": dram / alg, "source": NCU_TRAFFIC_PROFILE})
-    return out
 
 
-def run_syc53_sliced(args, rank, world, dev, depth=SYC_SLICED_DEPTH):
-    """One amplitude of the 53-qubit Sycamore circuit at ``depth`` cycles
-    through the reference's slicing scheme (network.py:385-455: cut edges fixed
-    per slice, slices summed): unsliced, the network needs 2^35-element
-    intermediates; with the two cut edges it runs as 64 slices of at most 2^31
-    elements, one slice per device pass, summed on the device.  With N ranks
-    the 64 slices are split over the ranks (distributed.sharded_amplitudes)
-    and one NCCL all-reduce sums them (strong scaling: one amplitude)."""
+# ---------------------------------------------------------------------------
+# headline: 53q depth 12, two-sided, sliced
+# ---------------------------------------------------------------------------
+def d12_engine(dev, max_batch_elems=1):
+    from paper_2011_02621_b200.network import TwoSidedEngine
+
+    circ = syc_circuit(D12["depth"])
+    return TwoSidedEngine(circ, split_cycle=D12["split"], cuts=D12["cuts"], max_rank=D12["cap"],
+                          dtype="complex64", device=dev, max_batch_elems=max_batch_elems), circ
+
+
+def d12_config(eng=None, k=1):
+    cfg = {"workload": "configs[4]: 53-qubit Sycamore (ABCDCDAB, fSim(pi/2, pi/6)), 12 cycles, two-sided split 6, "
+                       "rank cap 12, sliced over (45,49),(38,45); one step = 1 bitstring x "
+                       f"{k} slice(s) per rank",
+           "dtype": "complex64", "depth": 12, "split_cycle": 6, "max_rank": 12,
+           "cut_edges": [list(e) for e in D12["cuts"]], "slices_per_amplitude": 1024,
+           "slices_per_step_per_rank": k, "circuit_seed": SEED,
+           "l2": "inputs larger than L2 (2 x 2^31-element complex64 ping-pong accumulators)"}
+    return cfg
+
+
+def d12_plan_info(eng):
+    return {"multiplies_per_amplitude": eng.plan.multiplies, "max_elems": eng.plan.max_elems,
+            "path_steps": len(eng.plan.steps), "path": list(eng.path), "path_score": str(eng.path_score)}
+
+
+def run_d12(args, rank, world, dev):
     import torch
 
-    from paper_2011_02621_b200 import AmplitudeEngine, pattern_rqc, sycamore53_graph
-    from paper_2011_02621_b200.distributed import sharded_amplitudes
-
+    hbm, bf16, bf16_sus, peak_src = peaks()
     t0 = time.perf_counter()
-    graph, pats, _ = sycamore53_graph()
-    circ = pattern_rqc(graph, [pats[c] for c in "ABCDCDAB"], depth, seed=0)
-    eng = AmplitudeEngine(circ, dtype="complex64", max_rank=SYC_MAX_RANK, cuts=SYC_SLICED_CUTS,
-                          max_batch_elems=1, device=dev)
+    eng, circ = d12_engine(dev)
+    bits = random_bits(53, 1, 100)
+    ex = eng.prepare(bits)
     setup_s = time.perf_counter() - t0
-    ex, plan = eng.executor, eng.plan
-    rng = np.random.default_rng(100)
-    bits = rng.integers(0, 2, (1, 53)).astype(np.int32)
-    sel = eng.selectors(bits)
+    plan = eng.plan
+    S = plan.slice_count
+    k = args.slices_per_step
     amp = torch.zeros(1, dtype=torch.complex64, device=dev)
-
-    def one_pass():
-        amp.zero_()
-        if world > 1:
-            sharded_amplitudes(ex, sel, 1, amp)
-        else:
-            eng.amplitudes_device(sel, 1, amp)
-
     stream = torch.cuda.current_stream(dev)
-    for _ in range(args.warmup):
-        one_pass()
+
+    def slice_range(i):
+        lo = ((i * world + rank) * k) % S
+        return range(lo, min(lo + k, S))
+
+    def one_step(i):
+        amp.zero_()
+        eng.run(ex, 1, amp, slices=slice_range(i))
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.all_reduce(amp)                   # slice sum across ranks (NCCL)
+
+    for i in range(args.warmup):
+        one_step(i)
     barrier(world)
     torch.cuda.synchronize(dev)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(dev.index) as clk:
-        for e0, e1 in evs:
+        for i, (e0, e1) in enumerate(evs):
             e0.record(stream)
-            one_pass()
+            one_step(args.warmup + i)
             e1.record(stream)
         torch.cuda.synchronize(dev)
     t = sum(e0.elapsed_time(e1) for e0, e1 in evs) * 1e-3
     barrier(world)
     t_max = allreduce_max(t, world, dev)
+    value = world * k * args.steps / S / t_max
+    times = step_times(ex, plan, dev)
+    roof = path_roofline(plan, times, 1, 8, hbm, bf16, bf16_sus)
+    roof["peak_source"] = f"{peak_src} bf16_tflops (MEASURED_PEAKS.json, burst); sustained {bf16_sus}"
+    nt = ncu_traffic()
+    roof["traffic"] = nt.get("dram_bytes") if nt else None
+    if nt:
+        roof["traffic_check"] = nt
+    top = sorted(zip(plan.steps, times), key=lambda x: -x[1])[:6]
     res = {
-        "value": args.steps / t_max, "unit": "amplitudes/s", "ms_per_step": 1e3 * t_max / args.steps,
-        "scaling": "strong", "tflops_complex64_work": 8 * plan.multiplies * args.steps / t_max / 1e12,
-        "config": {"workload": f"configs[4] circuit family: 53-qubit Sycamore, ABCDCDAB, {depth} cycles, "
-                               f"sliced over cut edges {SYC_SLICED_CUTS} ({plan.slice_count} slices)",
-                   "dtype": "complex64", "bitstrings_per_step": 1, "slices": plan.slice_count,
-                   "multiplies_per_amplitude": plan.multiplies, "max_elems": plan.max_elems,
-                   "path_steps": len(plan.steps), "host_setup_s": setup_s,
-                   "sharding": ("slices split over ranks + one NCCL all_reduce(sum)" if world > 1
-                                else "single GPU, one slice per device pass, device slice sum"),
-                   "l2": "inputs larger than L2 (2 x 16 GiB ping-pong buffers)"},
-        "clocks": clk.summary(), "dtype": "complex64", "steps": args.steps, "warmup": args.warmup,
+        "value": value, "unit": "amplitudes/s", "ms_per_step": 1e3 * t_max / args.steps,
+        "s_per_amplitude_per_gpu": t_max / args.steps * S / k,
+        "gpu_launches": launches_per_pass(plan, 1) * k * args.steps,
+        "roofline": roof, "config": d12_config(None, k), "plan": d12_plan_info(eng), "clocks": clk.summary(),
+        "dtype": "complex64",
+        "host_setup_s": setup_s,
+        "sharding": ("rank r contracts slices (i*W + r)*k.. of step i; one NCCL all_reduce(sum) per step = the "
+                     "slice sum" if world > 1 else "single GPU"),
+        "top_steps": [{"M": sp.M, "K": sp.K, "N": sp.N, "ms": 1e3 * tt, "tflops": 8e-12 * sp.M * sp.K * sp.N / tt}
+                      for sp, tt in top],
     }
-    if args.e2e and world == 1:
-        outs = ["".join(map(str, row)) for row in bits]
+    if args.e2e:
+        # through the public API with host buffers: host bitstring in, bra
+        # evolution + overlap sites (H2D), the step's slices, host amplitude out
+        h2d = sum(t.data.nbytes for t in eng.phi.tensors.values())
+        pb = eng.bra_batch(bits)
+        h2d += sum(t.nbytes for t in pb.tensors.values()) + 53
+        steps = max(1, min(args.steps, 3))
+        eng.amplitudes(bits, slices=slice_range(0))
+        torch.cuda.synchronize(dev)
+        barrier(world)
         t0 = time.perf_counter()
-        eng.amplitudes(outs, graph=False)
-        te = time.perf_counter() - t0
-        res["e2e"] = {"value": 1.0 / te, "unit": "amplitudes/s", "h2d_bytes_per_step": 53 * 4,
-                      "d2h_bytes_per_step": 8, "steps": 1,
-                      "path": "AmplitudeEngine.amplitudes(list of bitstring strings, graph=False) -> host complex array"}
-    res["_plan_steps"] = [(sp.M, sp.K, sp.N) for sp in plan.steps]
-    res["_slices"] = plan.slice_count
+        for i in range(steps):
+            a = eng.amplitudes(bits, slices=slice_range(i))
+            if world > 1:
+                import torch.distributed as dist
+
+                ta = torch.from_numpy(a).to(dev)
+                dist.all_reduce(ta)
+        te = allreduce_max(time.perf_counter() - t0, world, dev)
+        res["e2e"] = {"value": world * k * steps / S / te, "unit": "amplitudes/s", "h2d_bytes_per_step": h2d,
+                      "d2h_bytes_per_step": 16, "steps": steps,
+                      "path": "TwoSidedEngine.amplitudes([bitstring], slices=...) -> host complex partial amplitude "
+                              "(host bra evolution, overlap sites built on the GPU, the slices, D2H)"}
+    res["_engine"] = eng
     return res
 
 
-def syc_plan_shapes_host(depth=SYC_DEPTH):
-    """(M, K, N) of every path step, computed on the host only (circuit, TNS
-    evolution, path search, plan) -- for the CPU reference arm."""
-    from paper_2011_02621_b200 import pattern_rqc, sycamore53_graph
-    from paper_2011_02621_b200 import network as NW
-    from paper_2011_02621_b200.circuit import fuse_single_qubit_gates
-    from paper_2011_02621_b200.engine import ContractionPlan, NetworkSpec
-    from paper_2011_02621_b200.tns import evolve, init_state
-
-    graph, pats, _ = sycamore53_graph()
-    circ = pattern_rqc(graph, [pats[c] for c in "ABCDCDAB"], depth, seed=0)
-    fused = fuse_single_qubit_gates(circ)
-    phi = evolve(init_state(fused.graph, "0" * 53), fused, range(fused.depth), "forward", 1e-12)
-    edges = {e: phi.bond_dims[e] for e in fused.graph.edges}
-    path, _ = NW._path_for(NW._ShapeNet(range(53), edges), NW.CutPlan((), ()), SYC_MAX_RANK)
-    legs = {q: fused.graph.node_edges(q) for q in range(53)}
-    plan = ContractionPlan(NetworkSpec(list(range(53)), edges, legs), path)
-    return [(sp.M, sp.K, sp.N) for sp in plan.steps]
-
-
-def cpu_syc_rate(step_shapes, budget_s: float = 20.0):
-    """CPU time per amplitude for the syc53 path, estimated from the oracle's
-    contraction primitive (numpy tensordot, as tnsim.tensor.contract_pair) on
-    row samples of every distinct step shape (M_s = min(M, 2^14) rows of
-    [M, K] x [K, N], complex64), scaled by M / M_s."""
-    rng = np.random.default_rng(0)
-    shapes = sorted(set((K, N) for _, K, N in step_shapes), key=lambda x: -x[0] * x[1])
-    per_row = {}
-    t_start = time.perf_counter()
-    for K, N in shapes:
-        ms = 1 << 14
-        a = (rng.standard_normal((ms, K)) + 1j * rng.standard_normal((ms, K))).astype(np.complex64)
-        b = (rng.standard_normal((K, N)) + 1j * rng.standard_normal((K, N))).astype(np.complex64)
-        reps, t0 = 0, time.perf_counter()
-        while True:
-            np.tensordot(a, b, axes=([1], [0]))
-            reps += 1
-            if time.perf_counter() - t0 > min(1.0, budget_s / len(shapes)) or reps >= 20:
-                break
-        per_row[(K, N)] = (time.perf_counter() - t0) / reps / ms
-        if time.perf_counter() - t_start > budget_s:
-            break
-    worst = max(per_row.values())
-    t_amp = sum(M * per_row.get((K, N), worst) for M, K, N in step_shapes)
-    return 1.0 / t_amp, time.perf_counter() - t_start
-
-
-def run_cfg0(args, rank, world, dev):
-    import torch
-
-    from paper_2011_02621_b200 import AmplitudeEngine, generate_lattice, pattern_rqc, square_patterns
-
-    g = generate_lattice("square", 3, 3)
-    circ = pattern_rqc(g, square_patterns(3, 3), 8, seed=0)
-    eng = AmplitudeEngine(circ, "0" * 9, dtype="complex128", device=dev)
-    rng = np.random.default_rng(rank)
-    B = 64
-    bits = rng.integers(0, 2, (B, 9)).astype(np.int32)
-    sel = eng.selectors(bits)
-    amp = torch.zeros(B, dtype=torch.complex128, device=dev)
-    stream = torch.cuda.current_stream(dev)
-    for _ in range(args.warmup):
-        eng.amplitudes_device(sel, B, amp, graph=True)
-    barrier(world)
-    torch.cuda.synchronize(dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev.index) as clk:
-        e0.record(stream)
-        for _ in range(args.steps):
-            eng.amplitudes_device(sel, B, amp, graph=True)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-    t = allreduce_max(e0.elapsed_time(e1) * 1e-3, world, dev)
-    # e2e: host bitstrings in, host amplitudes out, through the public API
-    outs = ["".join(map(str, row)) for row in bits]
-    for _ in range(2):                           # eager, then graph capture (untimed)
-        eng.amplitudes(outs)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        eng.amplitudes(outs)
-    te = allreduce_max(time.perf_counter() - t0, world, dev)
-    hbm, _, src = peaks()
-    return {"value": world * B * args.steps / t, "unit": "amplitudes/s", "ms_per_step": 1e3 * t / args.steps,
-            "gpu_launches": eng.executor.launches_per_chunk() * args.steps,
-            "roofline": {"bound": "latency", "achieved": None, "peak": hbm, "unit": "GB/s", "frac": None,
-                         "traffic": None, "note": "9-qubit network: launch-bound; every pass replays one "
-                                                  "CUDA graph of the whole path (projection, steps, slice sum)"},
-            "config": {"workload": "configs[0] 3x3 square, 8 cycles, 64 bitstrings", "dtype": "complex128",
-                       "l2": "inputs L2-resident (tiny network)"},
-            "clocks": clk.summary(), "dtype": "complex128",
-            "e2e": {"value": world * B * args.steps / te, "unit": "amplitudes/s", "h2d_bytes_per_step": B * 9 * 4,
-                    "d2h_bytes_per_step": B * 16}}
-
-
-# ---------------------------------------------------------------------------
-# CPU reference arm (oracle port of tnsim's numpy tensordot path)
-# ---------------------------------------------------------------------------
-def cpu_sweep_rates(budget_s: float = 20.0):
-    """Per-(k, n) CPU throughput (bytes/s of algorithmic traffic) of the
-    oracle port, measured on r = 16..20, B = 1 cases within ``budget_s``."""
+def cpu_d12(work_cap=1e9, groups=None):
+    """CPU reference of one d12 slice: the reference's np.tensordot steps on
+    its own operand layouts (oracle, complex64, all host threads), each path
+    step on a row subset of ~work_cap multiplies scaled by the row ratio."""
     sys.path.insert(0, str(ROOT / "oracle"))
     import tn_oracle as O
 
-    try:
-        from threadpoolctl import threadpool_info
+    from paper_2011_02621_b200.circuit import fuse_single_qubit_gates
+    from paper_2011_02621_b200.network import _path_for, _resolve_cuts, _ShapeNet
+    from paper_2011_02621_b200.tns import evolve, init_state, psi_batch
 
-        threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
-    except Exception:
-        threads = os.cpu_count() or 1
-    rng = np.random.default_rng(0)
-    rates = {}
-    t_start = time.perf_counter()
-    per_class = budget_s / 9
-    for k in (1, 2, 3):
-        for n in (1, 2, 3):
-            r = 18
-            perm, dims, pairs = case_layout(r, k, n, seed=k * 10 + n)
-            acc = (rng.standard_normal((1, 2 ** r * 4 ** k)) + 1j * rng.standard_normal((1, 2 ** r * 4 ** k))).astype(np.complex64)
-            site = (rng.standard_normal((2,) + (4,) * (k + n)) + 1j * rng.standard_normal((2,) + (4,) * (k + n))).astype(np.complex64)
-            bits = np.zeros(1, dtype=np.int64)
-            reps, t0 = 0, time.perf_counter()
-            while True:
-                O.sweep_step(acc, perm, r, k, site, bits)
-                reps += 1
-                el = time.perf_counter() - t0
-                if el > per_class or reps >= 50:
-                    break
-            by, _ = case_traffic(r, k, n, 1)
-            rates[(k, n)] = by * reps / el
-    return rates, threads, time.perf_counter() - t_start
+    circ = syc_circuit(D12["depth"])
+    fused = fuse_single_qubit_gates(circ)
+    phi = evolve(init_state(fused.graph, "0" * 53), fused, range(0, D12["split"]), "forward")
+    psi = psi_batch(fused, ["0" * 53], D12["split"])
+    edges = {e: phi.bond_dims[e] * psi.bond_dims[e] for e in fused.graph.edges}
+    sn = _ShapeNet(range(53), edges)
+    plan = _resolve_cuts(sn, D12["cuts"], D12["cap"])
+    path, _ = _path_for(sn, plan, D12["cap"])
+    legs = {q: fused.graph.node_edges(q) for q in range(53)}
+    lay = O.reference_step_layouts(legs, edges, path, plan.cut_edges)
+    return lay, edges, plan.slice_count, O
 
 
-def _cpu_threads():
+def _threads():
     try:
         from threadpoolctl import threadpool_info
 
@@ -721,168 +446,483 @@ def _cpu_threads():
         return os.cpu_count() or 1
 
 
-def cpu_value_for(cases, rates):
-    t = sum(case_traffic(*c)[0] / rates[(c[1], c[2])] for c in cases)
-    return sum(c[3] for c in cases) / t
+# ---------------------------------------------------------------------------
+# nested: two-sided 53q at depth 8 / 10 (whole amplitudes, bitstring batches)
+# ---------------------------------------------------------------------------
+def run_twosided(args, rank, world, dev, depth, B, steps, warmup):
+    import torch
+
+    from paper_2011_02621_b200.network import TwoSidedEngine
+
+    hbm, bf16, bf16_sus, _ = peaks()
+    t0 = time.perf_counter()
+    circ = syc_circuit(depth)
+    eng = TwoSidedEngine(circ, split_cycle=depth // 2, max_rank=12, dtype="complex64", device=dev)
+    setup_s = time.perf_counter() - t0
+    bits = random_bits(53, B * world, 200 + depth)
+    mine = bits[rank * B:(rank + 1) * B]              # weak scaling: B bitstrings per rank
+    ex = eng.prepare(mine)
+    plan = eng.plan
+    amp = torch.zeros(B, dtype=torch.complex64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(warmup):
+        eng.run(ex, B, amp)
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    with ClockSampler(dev.index) as clk:
+        for e0, e1 in evs:
+            e0.record(stream)
+            eng.run(ex, B, amp)
+            e1.record(stream)
+        torch.cuda.synchronize(dev)
+    t = allreduce_max(sum(a.elapsed_time(b) for a, b in evs) * 1e-3, world, dev)
+    z = ex._steps[0].Z
+    times = step_times(ex, plan, dev)
+    roof = path_roofline(plan, times, z, 8, hbm, bf16, bf16_sus)
+    res = {"value": world * B * steps / t, "unit": "amplitudes/s", "ms_per_step": 1e3 * t / steps,
+           "scaling": "weak", "steps": steps, "warmup": warmup,
+           "gpu_launches": launches_per_pass(plan, z) * len(ex.chunks(B, range(plan.slice_count))) * steps,
+           "roofline": roof,
+           "config": {"workload": f"configs[4] circuit family: 53-qubit Sycamore, {depth} cycles, two-sided split "
+                                  f"{depth // 2} (reference default), rank cap 12, unsliced",
+                      "dtype": "complex64", "bitstrings_per_step_per_rank": B,
+                      "multiplies_per_amplitude": plan.multiplies, "max_elems": plan.max_elems,
+                      "path_steps": len(plan.steps), "host_setup_s": setup_s},
+           "clocks": clk.summary(), "dtype": "complex64"}
+    if args.e2e:
+        eng.amplitudes(mine)
+        torch.cuda.synchronize(dev)
+        barrier(world)
+        es = max(1, min(steps, 3))
+        t0 = time.perf_counter()
+        host_t = 0.0
+        for _ in range(es):
+            eng.amplitudes(mine)
+            host_t += eng.last_host_s
+        te = allreduce_max(time.perf_counter() - t0, world, dev)
+        pb = eng.bra_batch(mine[:1])
+        per_b = sum(v.nbytes for v in pb.tensors.values())
+        res["e2e"] = {"value": world * B * es / te, "unit": "amplitudes/s", "steps": es,
+                      "h2d_bytes_per_step": B * (per_b + 53) + sum(v.data.nbytes for v in eng.phi.tensors.values()),
+                      "d2h_bytes_per_step": B * 16, "host_bra_evolution_share": host_t / te,
+                      "path": "TwoSidedEngine.amplitudes(list of bitstrings) -> host amplitudes (batched host bra "
+                              "evolution, overlap sites on the GPU, contraction, D2H)"}
+    res["_engine"] = eng
+    return res
 
 
-def run_reference(args):
-    rates, threads, spent = cpu_sweep_rates(args.cpu_budget)
-    cases = sweep_cases(args.limit)
-    v = cpu_value_for(cases, rates)
-    return v, threads, spent
+def cpu_twosided(depth, n, budget_s):
+    """The reference CPU path measured on whole amplitudes: two-sided
+    evolution (host), overlap network and np.tensordot along the path (oracle,
+    complex128 as the reference)."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import tn_oracle as O
+
+    from paper_2011_02621_b200.circuit import fuse_single_qubit_gates
+    from paper_2011_02621_b200.network import _path_for, _resolve_cuts, _ShapeNet
+    from paper_2011_02621_b200.tns import two_sided_evolve
+
+    circ = syc_circuit(depth)
+    bits = random_bits(53, n, 300 + depth)
+    done, t0 = 0, time.perf_counter()
+    for ob in bits:
+        fused = fuse_single_qubit_gates(circ)
+        phi, psi = two_sided_evolve(fused, "0" * 53, ob, depth // 2)
+        edges = {e: phi.bond_dims[e] * psi.bond_dims[e] for e in fused.graph.edges}
+        sn = _ShapeNet(range(53), edges)
+        path, _ = _path_for(sn, _resolve_cuts(sn, None, 12), 12)
+        ne = {q: fused.graph.node_edges(q) for q in range(53)}
+        tens = O.overlap_tensors({q: (phi.tensors[q].data, list(phi.tensors[q].labels)) for q in range(53)},
+                                 {q: (psi.tensors[q].data, list(psi.tensors[q].labels)) for q in range(53)},
+                                 ne, phi.bond_dims, psi.bond_dims)
+        O.sliced_amplitude(tens, path)
+        done += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    el = time.perf_counter() - t0
+    return {"value": done / el, "unit": "amplitudes/s", "cores": _threads(), "kind": "port",
+            "sample": f"{done} whole amplitudes (two-sided evolution + overlap + np.tensordot path, complex128 "
+                      f"as the reference), {el:.1f} s"}
 
 
 # ---------------------------------------------------------------------------
-def barrier(world):
+# nested: configs[1] pairwise-contraction sweep
+# ---------------------------------------------------------------------------
+def sweep_cases(limit=SWEEP_LIMIT):
+    cases, dropped = [], []
+    for r in (16, 20, 24, 28):
+        for k in (1, 2, 3):
+            for n in (1, 2, 3):
+                for B in (1, 16, 256):
+                    (cases if B * (2 ** r) * (4 ** max(k, n)) <= limit else dropped).append((r, k, n, B))
+    return cases, dropped
+
+
+def case_layout(r, k, n, seed):
+    rng = np.random.default_rng(seed)
+    perm = [int(x) for x in rng.permutation(r + k)]
+    dims = [2 if x < r else 4 for x in perm]
+    shared_pos = sorted((i for i, x in enumerate(perm) if x >= r), key=lambda i: perm[i])
+    pairs = [(p, j) for j, p in enumerate(shared_pos)]
+    return perm, dims, pairs
+
+
+def case_traffic(r, k, n, B, itemsize=8):
+    acc = B * 2 ** r * 4 ** k
+    out = B * 2 ** r * 4 ** n
+    site = B * 4 ** (k + n)
+    return (acc + out + 2 * site) * itemsize, 8 * B * 2 ** r * 4 ** k * 4 ** n
+
+
+def run_sweep(args, rank, world, dev, steps, warmup):
+    """Every (r, k, n, B) case of configs[1] whose operands fit (<= 2^32
+    elements each): projection gather + fused permute/contract per case, each
+    case timed with CUDA events after an untimed L2 flush."""
+    import torch
+
+    from paper_2011_02621_b200.engine import PairPlan, project_variants
+
+    hbm, bf16, _, peak_src = peaks()
+    cases, dropped = sweep_cases(args.limit)
+    max_acc = max(B * 2 ** r * 4 ** k for r, k, n, B in cases)
+    max_out = max(B * 2 ** r * 4 ** n for r, k, n, B in cases)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    acc = torch.randn(max_acc, dtype=torch.complex64, device=dev, generator=g)
+    out = torch.empty(max_out, dtype=torch.complex64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush_f = flush.view(torch.float32)
+    sink = torch.empty((), dtype=torch.float32, device=dev)
+    plans, inputs = [], []
+    for ci, (r, k, n, B) in enumerate(cases):
+        perm, dims, pairs = case_layout(r, k, n, seed=ci)
+        plans.append(PairPlan(dims, [4] * (k + n), pairs, dtype="complex64"))
+        variants = torch.randn((2, 4 ** (k + n)), dtype=torch.complex64, device=dev, generator=g)
+        bits = torch.randint(0, 2, (B,), dtype=torch.int32, device=dev, generator=g)
+        inputs.append((variants, bits, torch.empty((B, 4 ** (k + n)), dtype=torch.complex64, device=dev)))
+    stream = torch.cuda.current_stream(dev)
+
+    def one_step():
+        per = []
+        for ci, (r, k, n, B) in enumerate(cases):
+            variants, bits, site = inputs[ci]
+            flush.zero_()
+            torch.sum(flush_f, dim=0, out=sink)
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record(stream)
+            project_variants(variants, bits, site, 4 ** (k + n), stream)
+            e1.record(stream)
+            plans[ci](acc, site, out, B, 2 ** r * 4 ** k, 4 ** (k + n), 2 ** r * 4 ** n, stream)
+            e2.record(stream)
+            per.append((e0, e1, e2))
+        torch.cuda.synchronize(dev)
+        return [(a.elapsed_time(c) * 1e-3, b.elapsed_time(c) * 1e-3) for a, b, c in per]
+
+    for _ in range(warmup):
+        one_step()
+    barrier(world)
+    with ClockSampler(dev.index) as clk:
+        rows = [one_step() for _ in range(steps)]
+    t_case = allreduce_max(sum(tc for st in rows for tc, _ in st), world, dev)
+    per_case_k = [sum(rows[s][ci][1] for s in range(steps)) / steps for ci in range(len(cases))]
+    t_kern = sum(per_case_k)
+    units = sum(B for *_, B in cases)
+    roof_t = sum(max(case_traffic(*c)[0] / (hbm * 1e9), case_traffic(*c)[1] / (bf16 * 1e12)) for c in cases)
+    by = sum(case_traffic(*c)[0] for c in cases)
+    res = {"value": world * units * steps / t_case, "unit": "bitstring-steps/s", "ms_per_step": 1e3 * t_case / steps,
+           "scaling": "weak", "steps": steps, "warmup": warmup, "gpu_launches": 2 * len(cases) * steps,
+           "roofline": {"bound": "hbm", "achieved": by / t_kern / 1e9, "peak": hbm, "unit": "GB/s",
+                        "frac": roof_t / t_kern, "traffic": None, "peak_source": f"{peak_src} hbm_gbs",
+                        "kernel": "all contraction launches (tnc::k_tc_c64, tnc::k_pair_pipe*); projections excluded",
+                        "algorithmic": "per case (acc + out + 2*projected site) * 8 B"},
+           "config": {"workload": "configs[1] pairwise-contraction sweep", "dtype": "complex64",
+                      "cases": len(cases), "operand_limit_elems": args.limit,
+                      "excluded_cases_over_limit": [list(c) for c in dropped],
+                      "l2": "256 MiB memset + read before every case, untimed"},
+           "clocks": clk.summary(), "dtype": "complex64",
+           "detail": [{"r": r, "k": k, "n": n, "B": B, "kernel_us": 1e6 * tk,
+                       "GBps": case_traffic(r, k, n, B)[0] / tk / 1e9} for (r, k, n, B), tk in zip(cases, per_case_k)]}
+    return res
+
+
+def cpu_sweep(args, detail, budget_s):
+    """The oracle's sweep step (np.tensordot per bitstring, as the
+    reference's contract_pair) run in full on the smaller sweep cases until
+    ``budget_s``; the GPU value on exactly those cases is reported beside."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import tn_oracle as O
+
+    cases, _ = sweep_cases(args.limit)
+    order = sorted(range(len(cases)), key=lambda i: case_traffic(*cases[i])[0])
+    rng = np.random.default_rng(0)
+    done, t_cpu, t0 = [], 0.0, time.perf_counter()
+    for ci in order:
+        r, k, n, B = cases[ci]
+        perm, dims, pairs = case_layout(r, k, n, seed=ci)
+        acc = np.full((B, 2 ** r * 4 ** k), 0.5 - 0.25j, dtype=np.complex64)
+        site = (rng.standard_normal((2,) + (4,) * (k + n)) + 1j).astype(np.complex64)
+        bits = rng.integers(0, 2, B)
+        s0 = time.perf_counter()
+        O.sweep_step(acc, perm, r, k, site, bits)
+        t_cpu += time.perf_counter() - s0
+        done.append(ci)
+        if time.perf_counter() - t0 > budget_s:
+            break
+    units = sum(cases[i][3] for i in done)
+    t_gpu = sum(detail[i]["kernel_us"] for i in done) * 1e-6
+    return {"value": units / t_cpu, "unit": "bitstring-steps/s", "cores": _threads(), "kind": "port",
+            "sample": f"oracle sweep_step run in full on the {len(done)} smallest of {len(cases)} cases "
+                      f"({t_cpu:.1f} s of CPU); not extrapolated to the other cases",
+            "gpu_kernel_value_same_cases": units / t_gpu if t_gpu else None}
+
+
+# ---------------------------------------------------------------------------
+# nested: configs[0]
+# ---------------------------------------------------------------------------
+def run_cfg0(args, rank, world, dev, steps):
+    import torch
+
+    from paper_2011_02621_b200 import AmplitudeEngine, generate_lattice, pattern_rqc, square_patterns
+
+    g = generate_lattice("square", 3, 3)
+    circ = pattern_rqc(g, square_patterns(3, 3), 8, seed=0)
+    eng = AmplitudeEngine(circ, "0" * 9, dtype="complex128", device=dev)
+    B = 64
+    rng = np.random.default_rng(rank)
+    bits = rng.integers(0, 2, (B, 9)).astype(np.int32)
+    sel = eng.selectors(bits)
+    amp = torch.zeros(B, dtype=torch.complex128, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(3):
+        eng.amplitudes_device(sel, B, amp, graph=True)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        eng.amplitudes_device(sel, B, amp, graph=True)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    t = allreduce_max(e0.elapsed_time(e1) * 1e-3, world, dev)
+    outs = ["".join(map(str, row)) for row in bits]
+    for _ in range(2):
+        eng.amplitudes(outs)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        eng.amplitudes(outs)
+    te = allreduce_max(time.perf_counter() - t0, world, dev)
+    return {"value": world * B * steps / t, "unit": "amplitudes/s", "ms_per_step": 1e3 * t / steps, "steps": steps,
+            "config": {"workload": "configs[0] 3x3 square, 8 cycles, 64 bitstrings, projected engine",
+                       "dtype": "complex128"},
+            "e2e": {"value": world * B * steps / te, "unit": "amplitudes/s", "h2d_bytes_per_step": B * 9 * 4,
+                    "d2h_bytes_per_step": B * 16}}
+
+
+def cpu_cfg0(budget_s=5.0):
+    """configs[0] on the CPU, whole amplitudes: the reference's default
+    two-sided compute_amplitude path restated by the oracle (complex128)."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import tn_oracle as O
+
+    from paper_2011_02621_b200 import generate_lattice, pattern_rqc, square_patterns
+    from paper_2011_02621_b200.circuit import fuse_single_qubit_gates
+    from paper_2011_02621_b200.network import _path_for, _resolve_cuts, _ShapeNet
+    from paper_2011_02621_b200.tns import two_sided_evolve
+
+    g = generate_lattice("square", 3, 3)
+    circ = pattern_rqc(g, square_patterns(3, 3), 8, seed=0)
+    bits = random_bits(9, 64, 1)
+    done, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < budget_s:
+        ob = bits[done % 64]
+        fused = fuse_single_qubit_gates(circ)
+        phi, psi = two_sided_evolve(fused, "0" * 9, ob, 4)
+        edges = {e: phi.bond_dims[e] * psi.bond_dims[e] for e in fused.graph.edges}
+        sn = _ShapeNet(range(9), edges)
+        plan = _resolve_cuts(sn, "auto", None)
+        path, _ = _path_for(sn, plan, None)
+        ne = {q: fused.graph.node_edges(q) for q in range(9)}
+        tens = O.overlap_tensors({q: (phi.tensors[q].data, list(phi.tensors[q].labels)) for q in range(9)},
+                                 {q: (psi.tensors[q].data, list(psi.tensors[q].labels)) for q in range(9)},
+                                 ne, phi.bond_dims, psi.bond_dims)
+        O.sliced_amplitude(tens, path, plan.cut_edges, plan.extents)
+        done += 1
+    el = time.perf_counter() - t0
+    return {"value": done / el, "unit": "amplitudes/s", "cores": _threads(), "kind": "port",
+            "sample": f"{done} whole amplitudes through the reference's default pipeline (two-sided, auto cuts), "
+                      f"{el:.1f} s"}
+
+
+# ---------------------------------------------------------------------------
+# reference arm (CPU oracle port, same config as the headline)
+# ---------------------------------------------------------------------------
+def run_reference(args, base):
+    """Each step is a bounded sample of the d12 workload on the host cores:
+    the reference's np.tensordot steps of one slice on row subsets (every
+    path step once per group rotation: the path's steps are split into
+    ``NG`` groups of similar sampled work and step i runs group i mod NG).
+    value = amplitudes/s from the mean sampled time per full rotation x 1024
+    slices; ms_per_step is the wall time of the steps actually run."""
+    t0 = time.perf_counter()
+    lay, edges, S, O = cpu_d12()
+    setup = time.perf_counter() - t0
+    NG = 4
+    work = [min(1e9, prod(int(edges[e]) for e in a if e not in sh) * prod(int(edges[e]) for e in s))
+            for a, s, sh in lay]
+    target = sum(work) / NG
+    groups, cur, acc = [], [], 0.0
+    for i, w in enumerate(work):
+        cur.append(i)
+        acc += w
+        if acc >= target and len(groups) < NG - 1:
+            groups.append(cur)
+            cur, acc = [], 0.0
+    if cur:
+        groups.append(cur)
+    NG = len(groups)
+    est = [[] for _ in range(NG)]
+    wall = []
+    for i in range(args.warmup + args.steps):
+        gi = i % NG
+        s0 = time.perf_counter()
+        tot, _, _ = O.time_sampled_path([lay[j] for j in groups[gi]], edges, work_cap=1e9)
+        if i >= args.warmup:
+            est[gi].append(tot)
+            wall.append(time.perf_counter() - s0)
+    full = [np.mean(e) for e in est if e]
+    t_slice = sum(full) * NG / len(full)
+    v = 1.0 / (t_slice * S)
+    cpu = {"value": v, "unit": "amplitudes/s", "cores": _threads(), "kind": "port",
+           "sample": f"per step one of {NG} groups of the 52 path steps of one slice, each np.tensordot on the "
+                     "reference's operand layout over a row subset of <= 1e9 multiplies, scaled by rows; "
+                     f"{S} slices per amplitude; {t_slice:.0f} s per slice", "host_setup_s": setup}
+    return dict(base, impl="reference", value=v, unit="amplitudes/s", dtype="complex64",
+                ms_per_step=1e3 * float(np.mean(wall)), config=d12_config(None, args.slices_per_step),
+                cpu_baseline=cpu, e2e={"value": v, "unit": "amplitudes/s", "h2d_bytes_per_step": 0,
+                                       "d2h_bytes_per_step": 0})
+
+
+# ---------------------------------------------------------------------------
+def dry_run(args, rank, world):
+    """Plumbing check without a GPU: rank layout, slice ranges, gloo all-reduce
+    of partial amplitudes, max-over-ranks timing -- no contraction."""
+    import torch
+
+    S, k = 1024, args.slices_per_step
+    t0 = time.perf_counter()
+    part = torch.zeros(2, dtype=torch.float64)
+    for i in range(args.steps):
+        lo = ((i * world + rank) * k) % S
+        part[0] += float(lo)
+        part[1] += 1.0
     if world > 1:
         import torch.distributed as dist
 
-        dist.barrier()
-
-
-def allreduce_max(x, world, dev):
-    if world == 1:
-        return x
-    import torch
-    import torch.distributed as dist
-
-    t = torch.tensor([x], dtype=torch.float64, device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+        dist.all_reduce(part)
+    t = allreduce_max(time.perf_counter() - t0, world, torch.device("cpu"))
+    return {"dry_run": True, "value": None, "unit": "amplitudes/s", "slices_covered": int(part[1].item()),
+            "slice_index_sum": int(part[0].item()), "ms_per_step": 1e3 * t / max(1, args.steps),
+            "config": d12_config(None, k)}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="sweep", choices=["sweep", "cfg0", "syc53"])
+    ap.add_argument("--workload", default="d12", choices=["d12", "d10", "d8", "sweep", "cfg0"])
+    ap.add_argument("--slices-per-step", type=int, default=1)
     ap.add_argument("--limit", type=int, default=SWEEP_LIMIT)
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     ap.add_argument("--no-cpu", dest="cpu", action="store_false")
-    ap.add_argument("--cpu-budget", type=float, default=20.0)
-    ap.add_argument("--no-syc", dest="syc", action="store_false",
-                    help="sweep workload: skip the nested 53-qubit amplitude measurement")
+    ap.add_argument("--no-nested", dest="nested", action="store_false")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--dry-run", action="store_true", help="launch/sharding plumbing only (CPU, gloo)")
     args = ap.parse_args()
+    self_launch(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
     base = {"metric": METRIC, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "data": "synthetic (seeded)"}
-
-    if args.impl == "reference" and args.workload == "syc53":
-        if rank != 0:
-            return
-        shapes = syc_plan_shapes_host()
-        v, spent = cpu_syc_rate(shapes, args.cpu_budget)
-        line = dict(base, impl="reference", value=v, unit="amplitudes/s", n_gpus=world, dtype="complex64",
-                    ms_per_step=1e3 / v,
-                    config={"workload": "configs[4] circuit family: 53-qubit Sycamore, ABCDCDAB, "
-                                        f"{SYC_DEPTH} cycles", "dtype": "complex64"},
-                    cpu_baseline={"value": v, "unit": "amplitudes/s", "cores": _cpu_threads(), "kind": "port",
-                                  "sample": f"numpy tensordot on 2^14-row samples of every distinct step shape, "
-                                            f"{spent:.1f}s; scaled by rows"},
-                    e2e={"value": v, "unit": "amplitudes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
-        print(json.dumps(line))
-        return
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "data": "synthetic (seeded circuits)"}
     if args.impl == "reference":
-        if rank != 0:
-            return
-        v, threads, spent = run_reference(args)
-        line = dict(base, impl="reference", value=v, unit="bitstring-steps/s", n_gpus=world, dtype="complex64",
-                    ms_per_step=1e3 * sum(c[3] for c in sweep_cases(args.limit)) / v,
-                    config={"workload": "configs[1] pairwise-contraction sweep", "dtype": "complex64"},
-                    cpu_baseline={"value": v, "unit": "bitstring-steps/s", "cores": threads, "kind": "port",
-                                  "sample": f"oracle sweep_step (numpy tensordot) at r=18, B=1 for every (k,n); "
-                                            f"{spent:.1f}s of CPU; scaled per case by algorithmic bytes"},
-                    e2e={"value": v, "unit": "bitstring-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
-        print(json.dumps(line))
+        if rank == 0:
+            print(json.dumps(run_reference(args, base)))
         return
+    rank, world, dev = dist_setup(args)
+    if args.dry_run:
+        res = dry_run(args, rank, world)
+        if rank == 0:
+            print(json.dumps(dict(base, **res)))
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+        return
+    import gc
 
     import torch
 
-    if world > 1:
-        import torch.distributed as dist
-
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
-    torch.cuda.set_device(dev)
     from paper_2011_02621_b200 import _native
 
     _native.require_device()
-    runner = {"sweep": run_sweep, "cfg0": run_cfg0, "syc53": run_syc53}[args.workload]
-    res = runner(args, rank, world, dev)
-    plan_steps = res.pop("_plan_steps", None)
-    syc = syc9 = syc10 = None
-    if args.workload == "sweep" and args.syc:
-        # the headline circuit family, measured beside the sweep: amplitudes/s of
-        # the 53-qubit Sycamore network at the deepest depth one GPU holds
-        sargs = argparse.Namespace(**vars(args))
-        sargs.steps, sargs.warmup = max(3, min(args.steps, 5)), max(3, args.warmup)
-        syc = run_syc53(sargs, rank, world, dev)
-        syc_steps = syc.pop("_plan_steps", None)
-        if rank == 0 and args.cpu and world == 1 and syc_steps:
-            cv, spent = cpu_syc_rate(syc_steps, min(args.cpu_budget, 10.0))
-            syc["cpu_baseline"] = {"value": cv, "unit": "amplitudes/s", "cores": _cpu_threads(), "kind": "port",
-                                   "sample": f"numpy tensordot on 2^14-row samples of every distinct step shape, "
-                                             f"{spent:.1f}s; scaled by rows (permutation cost not included)"}
-        syc["steps"], syc["warmup"] = sargs.steps, sargs.warmup
-        # one cycle deeper: 6.7e12 multiplies and 2^31-element intermediates per
-        # amplitude (one amplitude per device pass), tensor-bound GEMM steps
-        import gc
 
-        gc.collect()
-        torch.cuda.empty_cache()                 # the depth-8 engine's buffers go back first
-        sargs9 = argparse.Namespace(**vars(sargs))
-        sargs9.steps = 3
-        syc9 = run_syc53(sargs9, rank, world, dev, depth=SYC_DEPTH + 1)
-        syc9_steps = syc9.pop("_plan_steps", None)
-        if rank == 0 and args.cpu and world == 1 and syc9_steps:
-            cv, spent = cpu_syc_rate(syc9_steps, min(args.cpu_budget, 10.0))
-            syc9["cpu_baseline"] = {"value": cv, "unit": "amplitudes/s", "cores": _cpu_threads(), "kind": "port",
-                                    "sample": f"numpy tensordot on 2^14-row samples of every distinct step shape, "
-                                              f"{spent:.1f}s; scaled by rows (permutation cost not included)"}
-        syc9["steps"], syc9["warmup"] = sargs9.steps, sargs9.warmup
-        # two cycles deeper, sliced (64 slices, 1.9e14 multiplies per amplitude)
+    def free(res):
+        if isinstance(res, dict):
+            res.pop("_engine", None)
         gc.collect()
         torch.cuda.empty_cache()
-        sargs10 = argparse.Namespace(**vars(sargs))
-        sargs10.steps, sargs10.warmup = 2, 1
-        syc10 = run_syc53_sliced(sargs10, rank, world, dev)
-        s10_steps, s10_slices = syc10.pop("_plan_steps", None), syc10.pop("_slices", 1)
-        if rank == 0 and args.cpu and world == 1 and s10_steps:
-            cv, spent = cpu_syc_rate(s10_steps, min(args.cpu_budget, 8.0))
-            syc10["cpu_baseline"] = {"value": cv / s10_slices, "unit": "amplitudes/s", "cores": _cpu_threads(),
-                                     "kind": "port",
-                                     "sample": f"numpy tensordot on 2^14-row samples of every distinct step shape, "
-                                               f"{spent:.1f}s; scaled by rows and by the {s10_slices} slices"}
+
+    cpu_here = rank == 0 and args.cpu and world == 1
+    if args.workload == "d12":
+        res = run_d12(args, rank, world, dev)
+        free(res)
+        if cpu_here:
+            lay, edges, S, O = cpu_d12()
+            tot, spent, _ = O.time_sampled_path(lay, edges, work_cap=1e9)
+            res["cpu_baseline"] = {"value": 1.0 / (tot * S), "unit": "amplitudes/s", "cores": _threads(),
+                                   "kind": "port",
+                                   "sample": "every path step of one slice once: np.tensordot on the reference's "
+                                             "operand layout over a row subset of <= 1e9 multiplies, scaled by rows "
+                                             f"({spent:.1f} s measured, {tot:.0f} s per slice); x{S} slices"}
+        nested = {}
+        if args.nested:
+            for depth, B in ((10, 8), (8, 64)):
+                r2 = run_twosided(args, rank, world, dev, depth, B, steps=5, warmup=3)
+                free(r2)
+                if cpu_here and depth == 8:         # a depth-10 amplitude takes minutes on the host
+                    r2["cpu_baseline"] = cpu_twosided(8, 2, 20.0)
+                nested[f"amplitudes_53q_depth{depth}_twosided"] = r2
+            r3 = run_sweep(args, rank, world, dev, steps=3, warmup=2)
+            if cpu_here:
+                r3["cpu_baseline"] = cpu_sweep(args, r3["detail"], 10.0)
+            r3.pop("detail", None)
+            free(None)
+            nested["sweep_configs1"] = r3
+            r4 = run_cfg0(args, rank, world, dev, steps=20)
+            if cpu_here:
+                r4["cpu_baseline"] = cpu_cfg0(5.0)
+            nested["configs0"] = r4
+        res.update(nested)
+    elif args.workload in ("d10", "d8"):
+        depth = int(args.workload[1:])
+        res = run_twosided(args, rank, world, dev, depth, 8 if depth == 10 else 64, args.steps, args.warmup)
+        free(res)
+        if cpu_here and depth == 8:
+            res["cpu_baseline"] = cpu_twosided(8, 2, 20.0)
+    elif args.workload == "sweep":
+        res = run_sweep(args, rank, world, dev, args.steps, args.warmup)
+        if cpu_here:
+            res["cpu_baseline"] = cpu_sweep(args, res["detail"], args.cpu_budget)
+        detail = res.pop("detail")
+        (ROOT / "gpurun_out").mkdir(exist_ok=True)
+        (ROOT / "gpurun_out" / "bench_detail.json").write_text(json.dumps(detail, indent=1))
+    else:
+        res = run_cfg0(args, rank, world, dev, args.steps)
+        if cpu_here:
+            res["cpu_baseline"] = cpu_cfg0(5.0)
     if rank == 0:
-        if args.cpu and world == 1:
-            if args.workload == "sweep":
-                rates, threads, spent = cpu_sweep_rates(args.cpu_budget)
-                cv = cpu_value_for(sweep_cases(args.limit), rates)
-                res["cpu_baseline"] = {"value": cv, "unit": "bitstring-steps/s", "cores": threads, "kind": "port",
-                                       "sample": f"oracle sweep_step (numpy) r=18, B=1 per (k,n), {spent:.1f}s; "
-                                                 "scaled per case by algorithmic bytes"}
-            elif args.workload == "syc53" and plan_steps:
-                cv, spent = cpu_syc_rate(plan_steps, args.cpu_budget)
-                res["cpu_baseline"] = {"value": cv, "unit": "amplitudes/s", "cores": _cpu_threads(), "kind": "port",
-                                       "sample": f"numpy tensordot (the oracle/reference contraction primitive) on "
-                                                 f"2^14-row samples of every distinct step shape, {spent:.1f}s; "
-                                                 "scaled by rows (permutation cost not included: favours the CPU)"}
-        detail = res.pop("detail", None)
-        line = dict(base, **res)
-        if syc is not None:
-            line["amplitudes_53q"] = syc
-            line["amplitudes_53q_depth9"] = syc9
-            line["amplitudes_53q_depth10_sliced"] = syc10
-        print(json.dumps(line))
-        if detail is not None:
-            (ROOT / "gpurun_out").mkdir(exist_ok=True)
-            (ROOT / "gpurun_out" / "bench_detail.json").write_text(json.dumps(detail, indent=1))
+        print(json.dumps(dict(base, **res), default=str))
     if world > 1:
         import torch.distributed as dist
 

@@ -183,3 +183,65 @@ def sweep_step(acc: np.ndarray, acc_perm: Sequence[int], r: int, k: int, site: n
         res = np.tensordot(a, s, axes=(shared_pos, list(range(k))))
         out.append(res.reshape(-1))
     return np.stack(out)
+
+
+# -- CPU reference timing on the bench's networks ----------------------------
+def reference_step_layouts(node_edges: dict, edges: dict, path: Sequence[int], cut_edges=()):
+    """Per path step, the operand layouts the reference's contract_along_path
+    (network.py:246-266) hands to np.tensordot for one slice: accumulator
+    labels in tensordot output order (free a axes, then free b axes,
+    tensor.py:103-119), the site's labels in node order, cut edges removed
+    (np.take in slice_network).  Returns [(acc_labels, site_labels, shared)]."""
+    cut = set(tuple(e) for e in cut_edges)
+    lab = {q: [e for e in node_edges[q] if tuple(e) not in cut] for q in node_edges}
+    acc = list(lab[path[0]])
+    out = []
+    for q in path[1:]:
+        t = lab[q]
+        shared = sorted(set(acc) & set(t))
+        out.append((list(acc), list(t), shared))
+        acc = [x for x in acc if x not in shared] + [x for x in t if x not in shared]
+    return out
+
+
+def time_sampled_path(layouts, edges: dict, dtype=np.complex64, work_cap: float = 2e8, seed: int = 0):
+    """CPU time of one slice contracted the reference's way (np.tensordot on
+    the reference layouts), estimated step by step: each step runs on a
+    sub-block of its accumulator (outermost free legs fixed until at most
+    ``work_cap`` complex multiplies remain -- a row subset of the step's GEMM)
+    and its time is scaled by the row ratio.  Returns (seconds per slice,
+    seconds measured, multiplies run)."""
+    import time
+
+    total = spent = 0.0
+    done = 0
+    for acc_l, site_l, shared in layouts:
+        dims = [int(edges[e]) for e in acc_l]
+        tdims = [int(edges[e]) for e in site_l]
+        free_idx = [i for i, e in enumerate(acc_l) if e not in shared]
+        full_rows = prod(dims[i] for i in free_idx) if free_idx else 1
+        kn = prod(tdims) if tdims else 1          # K * N of the step
+        rows_cap = max(1, int(work_cap // kn))
+        sdims = list(dims)
+        rows = full_rows
+        for i in free_idx:                       # fix outermost free legs first
+            if rows <= rows_cap:
+                break
+            rows //= sdims[i]
+            sdims[i] = 1
+            if rows < rows_cap:                  # keep part of this leg
+                keep = min(dims[i], max(1, rows_cap // rows))
+                sdims[i] = keep
+                rows *= keep
+        # operand values do not change a dense tensordot's time: cheap fills
+        a = np.full(sdims, 0.5 - 0.25j, dtype=dtype)
+        b = np.full(tdims, 0.25 + 0.5j, dtype=dtype)
+        ia = [acc_l.index(s) for s in shared]
+        ib = [site_l.index(s) for s in shared]
+        t0 = time.perf_counter()
+        np.tensordot(a, b, axes=(ia, ib))
+        dt = time.perf_counter() - t0
+        spent += dt
+        done += rows * kn
+        total += dt * full_rows / rows
+    return total, spent, done

@@ -69,8 +69,12 @@ struct GemmDesc {
   const int64_t* c_noff;         // [N]
 };
 
+// warps: converters [0, CONVW), epilogue [CONVW, MMA), MMA issuer, A and B producers;
+// 3M tiles: 8 converter + 8 epilogue warps (19), otherwise 15 warps in all
 constexpr int TG_THREADS = 15 * 32;
-constexpr int TG_EPI_WARP0 = 8, TG_MMA_WARP = 12, TG_APROD_WARP = 13, TG_BPROD_WARP = 14;
+constexpr int TG_THREADS_G3 = 19 * 32;
+constexpr int TG_EPI_WARP0 = 8;
+__host__ __device__ constexpr int tg_mma_warp(bool g3) { return g3 ? 16 : 12; }
 constexpr int TG_MAX_RS = 8, TG_MAX_BS = 8;
 constexpr int TG_EPI_PITCH = 16 * 8 + 16;      // staged row: 16 complex + 16 B pad
 
@@ -227,7 +231,7 @@ __device__ __forceinline__ uint32_t f16_idesc(int n_real) {
 // columns, re = T1 - T2, im = T3 - T1 - T2 in the epilogue: 9 instead of 12
 // N = NT MMA units per chunk (wide tiles, NT = 128, one accumulator stage)
 template <int KC, bool F16, bool G3 = false>
-__global__ void __launch_bounds__(TG_THREADS, 1)
+__global__ void __launch_bounds__(G3 ? TG_THREADS_G3 : TG_THREADS, 1)
 k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMap tmA) {
   static_assert(!F16 || KC == 16, "F16 mode needs 16-complex chunks (K = 16 per MMA)");
   static_assert(!G3 || F16, "3M products run on the fp16-split operands");
@@ -248,7 +252,8 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
   // warp roles: converters [0, CONVW), epilogue [CONVW, 12) in EPIG groups of
   // four (one per TMEM lane quadrant; groups split the columns), 12 MMA, 13/14
   // producers.  fp16 conversion is cheap, so F16 gives the epilogue 8 warps.
-  constexpr int CONVW = F16 ? 4 : 8;
+  constexpr int TG_MMA_WARP = tg_mma_warp(G3), TG_APROD_WARP = TG_MMA_WARP + 1, TG_BPROD_WARP = TG_MMA_WARP + 2;
+  constexpr int CONVW = (F16 && !G3) ? 4 : 8;
   constexpr int EPIW = TG_MMA_WARP - CONVW;
   constexpr int EPIG = EPIW / 4;
   // narrow tiles (NT <= 32, short epilogue per item, latency-bound): the
@@ -344,10 +349,33 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
       for (int c = 0; c < nchunk; ++c, ++j) {
         mbar_wait_spin(&rfull[rstage], rph);
         const uint32_t src = smem_u32(araw + (size_t)rstage * RAW_BYTES);
-        if constexpr (F16) {
+        if constexpr (G3) {
+          // warp (quadrant, half h): complex [8h, 8h + 8) of its 32 rows ->
+          // Ar, Ai, As = Ar + Ai, hi/lo fp16, two per TMEM column (4 per plane)
+          uint32_t rh[4], ih[4], sh[4], rl[4], il[4], sl[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t off = (uint32_t)(r * RB + 16 * (4 * h + q));
+            const uint32_t phys = off ^ (((off >> 7) & SWM) << 4);
+            float4 x;
+            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w) : "r"(src + phys));
+            split_f16x2(x.x * sA, x.z * sA, rh[q], rl[q]);
+            split_f16x2(x.y * sA, x.w * sA, ih[q], il[q]);
+            split_f16x2((x.x + x.y) * sA, (x.z + x.w) * sA, sh[q], sl[q]);
+          }
+          mbar_wait_spin(&aempty[astage], aph ^ 1);
+          tc_fence_after();
+          // stage layout: [Ar_hi | Ai_hi | As_hi | Ar_lo | Ai_lo | As_lo], 8 columns each
+          const uint32_t col = A0 + (uint32_t)astage * ACOLS + 4 * h;
+          tmem_st<4>(tmem + lane_base + col, rh);
+          tmem_st<4>(tmem + lane_base + col + 8, ih);
+          tmem_st<4>(tmem + lane_base + col + 16, sh);
+          tmem_st<4>(tmem + lane_base + col + 24, rl);
+          tmem_st<4>(tmem + lane_base + col + 32, il);
+          tmem_st<4>(tmem + lane_base + col + 40, sl);
+        } else if constexpr (F16) {
           // 16 complex -> 16 Ar and 16 Ai values, hi/lo fp16, two per TMEM column
           uint32_t rh[KC / 2], ih[KC / 2], rl[KC / 2], il[KC / 2];
-          uint32_t sh[G3 ? KC / 2 : 1], sl[G3 ? KC / 2 : 1];
 #pragma unroll
           for (int q = 0; q < KC / 2; ++q) {
             const uint32_t off = (uint32_t)(r * RB + 16 * q);
@@ -356,26 +384,17 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
             asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w) : "r"(src + phys));
             split_f16x2(x.x * sA, x.z * sA, rh[q], rl[q]);   // re of complex 2q, 2q+1
             split_f16x2(x.y * sA, x.w * sA, ih[q], il[q]);   // im
-            if constexpr (G3) split_f16x2((x.x + x.y) * sA, (x.z + x.w) * sA, sh[q], sl[q]);   // re + im
           }
           mbar_wait_spin(&aempty[astage], aph ^ 1);
           tc_fence_after();
-          // stage layout: [Ar_hi 8 | Ai_hi 8 | Ar_lo 8 | Ai_lo 8] columns (16 k each);
-          // 3M: [Ar_hi | Ai_hi | As_hi | Ar_lo | Ai_lo | As_lo]
+          // stage layout: [Ar_hi 8 | Ai_hi 8 | Ar_lo 8 | Ai_lo 8] columns (16 k each)
           const uint32_t col = A0 + (uint32_t)astage * ACOLS;
-          if constexpr (G3) {
-            tmem_st<KC / 2>(tmem + lane_base + col, rh);
-            tmem_st<KC / 2>(tmem + lane_base + col + 8, ih);
-            tmem_st<KC / 2>(tmem + lane_base + col + 16, sh);
-            tmem_st<KC / 2>(tmem + lane_base + col + 24, rl);
-            tmem_st<KC / 2>(tmem + lane_base + col + 32, il);
-            tmem_st<KC / 2>(tmem + lane_base + col + 40, sl);
-          } else {
-            tmem_st<KC / 2>(tmem + lane_base + col, rh);
-            tmem_st<KC / 2>(tmem + lane_base + col + 8, ih);
-            tmem_st<KC / 2>(tmem + lane_base + col + 16, rl);
-            tmem_st<KC / 2>(tmem + lane_base + col + 24, il);
-          }
+          tmem_st<KC / 2>(tmem + lane_base + col, rh);
+          tmem_st<KC / 2>(tmem + lane_base + col + 8, ih);
+          tmem_st<KC / 2>(tmem + lane_base + col + 16, rl);
+          tmem_st<KC / 2>(tmem + lane_base + col + 24, il);
+        }
+        if constexpr (F16) {
           tmem_wait_st();
           tc_fence_before();
           mbar_arrive_warp(&afull[astage]);
@@ -859,7 +878,7 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
       cudaFuncSetAttribute(k_tc_gemm<16, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       attr |= 1ull << (adev & 63);
     }
-    if (p.g3) k_tc_gemm<16, true, true><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm);
+    if (p.g3) k_tc_gemm<16, true, true><<<(unsigned)grid, TG_THREADS_G3, smem, s>>>(p, tm);
     else if (f16) k_tc_gemm<16, true><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm);
     else if (KC == 16) k_tc_gemm<16, false><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm);
     else k_tc_gemm<8, false><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm);

@@ -346,7 +346,6 @@ def test_sycamore53_sliced_matches_unsliced():
     """53-qubit Sycamore (ABCDCDAB, 8 cycles): the projected engine sliced over
     the bench's depth-10 cut edges (network.py:385-455 scheme: cut legs fixed
     per slice, device slice sum) against the unsliced network, complex64."""
-    import bench
     from paper_2011_02621_b200 import AmplitudeEngine, pattern_rqc, sycamore53_graph
 
     graph, pats, _ = sycamore53_graph()
@@ -354,7 +353,7 @@ def test_sycamore53_sliced_matches_unsliced():
     rng = np.random.default_rng(11)
     outs = ["".join(map(str, r)) for r in rng.integers(0, 2, (2, 53))]
     ref = AmplitudeEngine(circ, dtype="complex64", max_rank=12).amplitudes(outs, graph=False)
-    eng = AmplitudeEngine(circ, dtype="complex64", max_rank=12, cuts=bench.SYC_SLICED_CUTS)
+    eng = AmplitudeEngine(circ, dtype="complex64", max_rank=12, cuts=[(9, 14), (2, 9)])
     assert eng.plan.slice_count > 1
     got = eng.amplitudes(outs, graph=False)
     assert rel_l2(got, ref) <= 1e-4

@@ -74,7 +74,7 @@ def test_tc_pair_sweep_layouts(r, k, n, B, seed, noxor, monkeypatch):
     if noxor:
         monkeypatch.setenv("TNC_TC_NOXOR", "1")
     case = tuple(int(x) for x in seed.split(":")[1].split(","))
-    perm, dims, pairs = bench.case_layout(case[0], case[1], case[2], bench.sweep_cases().index(case))
+    perm, dims, pairs = bench.case_layout(case[0], case[1], case[2], bench.sweep_cases()[0].index(case))
     # keep the innermost legs (the tile's row/k bank pattern) and drop outer row legs
     drop = case[0] - r
     keep = [i for i, x in enumerate(perm) if not (x < case[0] and sum(1 for y in perm[:i] if y < case[0]) < drop)]

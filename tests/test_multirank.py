@@ -119,3 +119,22 @@ def test_gloo_two_ranks_match_single_process(golden_amplitudes):
         assert p.exitcode == 0
     for r in range(2):
         np.testing.assert_allclose(results[r], full, atol=1e-12)
+
+
+def test_bench_self_launch_two_ranks():
+    """bench.py --gpus 2 outside torchrun re-launches itself with two ranks
+    (gloo on CPU in --dry-run): the JSON line reports n_gpus 2 and both ranks'
+    slice ranges were summed by the all-reduce."""
+    import json
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    proc = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--dry-run", "--steps", "3"],
+                          capture_output=True, text=True, timeout=300, cwd=str(ROOT))
+    assert proc.returncode == 0, proc.stderr[-2000:]
+    line = json.loads([ln for ln in proc.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["dry_run"]
+    assert line["slices_covered"] == 6
+    assert line["slice_index_sum"] == sum(range(6))

@@ -124,13 +124,17 @@ def main():
                     help="beam search of this width (0: greedy); beams ranked by "
                          "log2(multiplies) + max(0, log2(largest) - target)")
     ap.add_argument("--max-cuts", type=int, default=6)
+    ap.add_argument("--init-cuts", default="", help="start from these cut edges, e.g. 45-49,38-45")
     args = ap.parse_args()
     edges, legs = network_shape(args.net, args.depth, args.split, args.rows, args.cols, args.seed)
     _init(edges, legs, args.cap)
     t0 = time.time()
     cur = evaluate([])
     print(f"unsliced: 2^{math.log2(cur['max_elems']):.1f} elems, {cur['multiplies']:.3e} mult", flush=True)
-    cuts = []
+    cuts = [tuple(int(x) for x in c.split("-")) for c in args.init_cuts.split(",")] if args.init_cuts else []
+    if cuts:
+        cur = evaluate(cuts)
+        print(f"initial {cuts}: 2^{math.log2(cur['max_elems']):.1f} elems, {cur['multiplies']:.3e} mult", flush=True)
     if args.beam:
         with Pool(args.procs, initializer=_init, initargs=(edges, legs, args.cap)) as pool:
             cur = beam_search(pool, edges, cur, args)
