@@ -104,10 +104,43 @@ void warp_step(const tnc_step_desc& d, cudaStream_t s) {
 }
 
 template <typename R>
-bool try_skinny(const tnc_step_desc& d, cudaStream_t s) {
+bool splitk(const tnc_step_desc& d, cudaStream_t s) {
+  using C = typename tnc::cplx<R>::T;
+  constexpr int BM = 64, BN = 32, BK = 16;
+  const int64_t rows = d.Z * d.M;
+  const int64_t tiles_n = (d.N + BN - 1) / BN;
+  const int64_t tiles = ((rows + BM - 1) / BM) * tiles_n;
+  int64_t splits = std::max<int64_t>(1, (148 * 8 + tiles - 1) / tiles);
+  int64_t ks = (d.K + splits - 1) / splits;
+  ks = (ks + BK - 1) / BK * BK;
+  splits = (d.K + ks - 1) / ks;
+  if (splits > 65535) return false;
+  tnc::pool_keep();
+  C* W = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&W), (size_t)splits * rows * d.N * sizeof(C), s) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  tnc::k_step_splitk<R, BM, BN, BK, 4, 2><<<dim3((unsigned)tiles, (unsigned)splits), (BM / 4) * (BN / 2), 0, s>>>(
+      d, tiles_n, ks, W);
+  tnc::k_splitk_reduce<R><<<grid_for(rows * d.N, 256), 256, 0, s>>>(d, splits, W);
+  cudaFreeAsync(W, s);
+  return true;
+}
+
+template <typename R>
+bool try_skinny(const tnc_step_desc& d, cudaStream_t s, bool& fused_amax) {
+  fused_amax = false;
   if (!d.a_rows_contig || !d.b_dense || d.conj_b) return false;
   if (d.Z * d.M > (int64_t)0x7fffffff * 128) return false;
   const int64_t N = d.N, K = d.K;
+  // few rows with a long K and real work: split-K register-blocked partials
+  // plus a fixed-order reduction (a warp per result re-reads the site block
+  // once per row: 11 ms for M = 1024, K = 32768, N = 64)
+  if (d.Z * d.M < 4096 && K >= 2048 && d.Z * d.M * N * K >= ((int64_t)1 << 26) &&
+      (d.site.sel == nullptr || d.Z == 1) && d.site.ncut == 0 && d.site.zstride == 0) {
+    if (splitk<R>(d, s)) return true;
+  }
   // few rows (path ends: tiny M, large K or N): one thread per result element
   if (d.Z * d.M < 4096) {
     if (K >= 256 && d.Z * d.M * N <= (int64_t)148 * 64 * 8)   // long K: a warp per result
@@ -120,6 +153,7 @@ bool try_skinny(const tnc_step_desc& d, cudaStream_t s) {
   if (sizeof(R) == 4 && N <= 16 && K * N < 256 && K >= 2 && K <= 64 && (K & (K - 1)) == 0 &&
       ((uintptr_t)d.acc % 16) == 0 && (d.acc_zstride % 2) == 0 && d.M < 0x7fffffffLL &&
       d.out_zstride < 0x7fffffffLL) {
+    fused_amax = true;                           // k_step_warp records amax_out itself
     switch (K) {
       case 2: warp_step<1>(d, s); return true;
       case 4: warp_step<2>(d, s); return true;
@@ -192,7 +226,7 @@ int launch_step_kernel(const tnc_step_desc& d, cudaStream_t s, bool& fused_amax)
     if (kernel == TNC_K_TC) return fail(TNC_E_UNSUPPORTED, "tnc_step: shape outside the tensor-core kernel envelope");
   }
   if (kernel == TNC_K_SKINNY || kernel == TNC_K_AUTO) {
-    if (try_skinny<R>(d, s)) return check_launch("tnc_step[skinny]");
+    if (try_skinny<R>(d, s, fused_amax)) return check_launch("tnc_step[skinny]");
     if (kernel == TNC_K_SKINNY) return fail(TNC_E_UNSUPPORTED, "tnc_step: shape outside the skinny kernel envelope");
   }
   if (d.a_koff == nullptr || d.b_koff == nullptr || d.b_noff == nullptr || d.c_noff == nullptr)

@@ -33,14 +33,25 @@ k_project(const __grid_constant__ tnc_project_desc d, int64_t elems) {
 }
 
 // mixed-radix row decomposition -> (acc offset, out offset)
+// Mixed-radix row decomposition.  Leg extents are products of bond
+// dimensions, almost always powers of two: those legs take a mask and a shift
+// (the branch is warp-uniform, extents come from the descriptor) instead of a
+// 64-bit division, which dominated the SIMT steps' instruction count.
 __device__ __forceinline__ void row_offsets(const tnc_step_desc& d, int64_t f, int64_t& oa, int64_t& oc) {
   oa = 0; oc = 0;
   for (int j = d.nf - 1; j >= 0; --j) {
-    const int64_t q = f / d.f_dim[j];
-    const int64_t r = f - q * d.f_dim[j];
+    const int64_t dm = d.f_dim[j];
+    int64_t r;
+    if ((dm & (dm - 1)) == 0) {
+      r = f & (dm - 1);
+      f >>= (__ffsll(dm) - 1);
+    } else {
+      const int64_t q = f / dm;
+      r = f - q * dm;
+      f = q;
+    }
     oa += r * d.f_astride[j];
     oc += r * d.f_cstride[j];
-    f = q;
   }
 }
 
@@ -323,6 +334,106 @@ k_step_dot(const __grid_constant__ tnc_step_desc d) {
 }
 
 // ---------------------------------------------------------------------------
+// Split-K step for few rows and a long contracted extent (path ends: e.g.
+// M = 1024, K = 32768, N = 64): every CTA computes a BM x BN register-blocked
+// partial product over one K range of rows-contiguous A and a dense site
+// block into a workspace W[split][row][n]; k_splitk_reduce sums the splits
+// in a fixed order (bit-reproducible) and scatters through the row map.
+// ---------------------------------------------------------------------------
+template <typename R, int BM, int BN, int BK, int TM, int TN>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN))
+k_step_splitk(const __grid_constant__ tnc_step_desc d, int64_t tiles_n, int64_t ks,
+              typename cplx<R>::T* __restrict__ W) {
+  using C = typename cplx<R>::T;
+  constexpr int TX = BN / TN, TY = BM / TM, NT = TX * TY;
+  __shared__ C As[BK][BM + 1];
+  __shared__ C Bs[BK][BN + 1];
+  const int64_t rows = d.Z * d.M;
+  const int64_t r0 = (blockIdx.x / tiles_n) * BM, n0 = (blockIdx.x % tiles_n) * BN;
+  const int64_t k_begin = blockIdx.y * ks, k_end = min(k_begin + ks, d.K);
+  const int tx = threadIdx.x % TX, ty = threadIdx.x / TX;
+  C acc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j] = czero<R>();
+  for (int64_t k0 = k_begin; k0 < k_end; k0 += BK) {
+    for (int e = threadIdx.x; e < BM * BK; e += NT) {
+      const int i = e / BK, kk = e % BK;              // consecutive threads: consecutive k of one row
+      const int64_t row = r0 + i, k = k0 + kk;
+      C v = czero<R>();
+      if (row < rows && k < k_end) {
+        const int64_t z = row / d.M, f = row - z * d.M;
+        v = reinterpret_cast<const C*>(d.acc)[z * d.acc_zstride + f * d.K + k];
+      }
+      As[kk][i] = v;
+    }
+    for (int e = threadIdx.x; e < BK * BN; e += NT) {
+      const int kk = e / BN, j = e % BN;
+      const int64_t k = k0 + kk, n = n0 + j;
+      C v = czero<R>();
+      if (k < k_end && n < d.N) {
+        // one site block per z: the tile's rows may span z (same site unless
+        // variants / slices differ, handled by the caller: Z * M rows share it)
+        v = reinterpret_cast<const C*>(d.site.ptr)[site_offset(d.site, r0 / d.M, d.slices_per_b, d.s0) + k * d.N + n];
+        if (d.conj_b) v = cconj(v);
+      }
+      Bs[kk][j] = v;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int kk = 0; kk < BK; ++kk) {
+      C a[TM], b[TN];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) a[i] = As[kk][ty * TM + i];
+#pragma unroll
+      for (int j = 0; j < TN; ++j) b[j] = Bs[kk][tx + j * TX];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) cfma(acc[i][j], a[i], b[j]);
+    }
+    __syncthreads();
+  }
+  C* Wp = W + (int64_t)blockIdx.y * rows * d.N;
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int64_t row = r0 + ty * TM + i;
+    if (row >= rows) continue;
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int64_t n = n0 + tx + j * TX;
+      if (n < d.N) Wp[row * d.N + n] = acc[i][j];
+    }
+  }
+}
+
+template <typename R>
+__global__ void __launch_bounds__(256)
+k_splitk_reduce(const __grid_constant__ tnc_step_desc d, int64_t splits, const typename cplx<R>::T* __restrict__ W) {
+  using C = typename cplx<R>::T;
+  const int64_t rows = d.Z * d.M, total = rows * d.N;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    C v = czero<R>();
+    for (int64_t s = 0; s < splits; ++s) {
+      const C w = W[s * total + e];
+      v.x += w.x;
+      v.y += w.y;
+    }
+    const int64_t row = e / d.N, n = e - row * d.N;
+    const int64_t z = row / d.M, f = row - z * d.M;
+    C* o = reinterpret_cast<C*>(d.out) + z * d.out_zstride;
+    if (d.c_rows_contig) {
+      o[f * d.N + n] = v;
+    } else {
+      int64_t oa, oc;
+      row_offsets(d, f, oa, oc);
+      o[oc + d.c_noff[n]] = v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Warp-cooperative skinny step (complex64, K = 2L in {2..64}, N <= NN <= 4):
 // L lanes share one acc row, each loading 16 contiguous bytes (two complex),
 // so every warp load is a coalesced 512-byte stream of 32/L whole rows; the
@@ -334,9 +445,14 @@ __device__ __forceinline__ uint32_t row_cout32(const tnc_step_desc& d, uint32_t 
   uint32_t oc = 0;
   for (int j = d.nf - 1; j >= 0; --j) {
     const uint32_t dm = (uint32_t)d.f_dim[j];
-    const uint32_t q = f / dm;
-    oc += (f - q * dm) * (uint32_t)d.f_cstride[j];
-    f = q;
+    if ((dm & (dm - 1)) == 0) {                  // power-of-two leg: mask + shift
+      oc += (f & (dm - 1)) * (uint32_t)d.f_cstride[j];
+      f >>= (__ffs(dm) - 1);
+    } else {
+      const uint32_t q = f / dm;
+      oc += (f - q * dm) * (uint32_t)d.f_cstride[j];
+      f = q;
+    }
   }
   return oc;
 }
@@ -357,6 +473,7 @@ k_step_warp(const __grid_constant__ tnc_step_desc d) {
   const uint32_t wbase = (blockIdx.x * wpb + (threadIdx.x >> 5)) * RP * UNR;
   // results n0 .. n0 + OWN - 1 of each row end up in this lane
   const int n0 = NN >= L ? j * OWN : j;
+  float vmax = 0.f;
   for (int64_t z = blockIdx.y; z < d.Z; z += gridDim.y) {
     const float4* Az = reinterpret_cast<const float4*>(reinterpret_cast<const float2*>(d.acc) + z * d.acc_zstride);
     float2* Oz = reinterpret_cast<float2*>(d.out) + z * d.out_zstride;
@@ -422,8 +539,22 @@ k_step_warp(const __grid_constant__ tnc_step_desc d) {
         }
         const uint32_t f = base + u * RP + rg;
         if (f < M && n0 < N) {
-          if (d.c_rows_contig) {
-            float2* o = Oz + (size_t)f * N + n0;
+          if (d.amax_out) {
+#pragma unroll
+            for (int i = 0; i < OWN; ++i)
+              if (n0 + i < N) vmax = fmaxf(vmax, fmaxf(fabsf(v[i].x), fabsf(v[i].y)));
+          }
+          if (d.c_rows_contig || d.c_n_contig) {
+            // the lane's OWN results are consecutive in the row: 16-byte stores
+            float2* o = Oz + (d.c_rows_contig ? (size_t)f * N : (size_t)row_cout32(d, f)) + n0;
+            if constexpr (OWN >= 2) {
+              if ((OWN & 1) == 0 && n0 + OWN <= N) {
+#pragma unroll
+                for (int i = 0; i < OWN; i += 2)
+                  *reinterpret_cast<float4*>(o + i) = make_float4(v[i].x, v[i].y, v[i + 1].x, v[i + 1].y);
+                continue;
+              }
+            }
 #pragma unroll
             for (int i = 0; i < OWN; ++i)
               if (n0 + i < N) o[i] = v[i];
@@ -435,6 +566,11 @@ k_step_warp(const __grid_constant__ tnc_step_desc d) {
           }
         }
       }
+    }
+    if (d.amax_out) {                              // max |re|, |im| of out[z] for the next fp16-split GEMM step
+      for (int o = 16; o; o >>= 1) vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+      if (lane == 0 && vmax > 0.f) atomicMax(reinterpret_cast<unsigned int*>(d.amax_out) + z, __float_as_uint(vmax));
+      vmax = 0.f;
     }
   }
 }

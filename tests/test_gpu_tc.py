@@ -263,7 +263,9 @@ def test_tc_gemm_f16_split_step(M, K, N, scale, sscale):
 
 @pytest.mark.parametrize("dtype", ["complex64", "complex128"])
 @pytest.mark.parametrize("M,K,N", [(65536, 16, 1), (65536, 8, 4), (65536, 2, 2), (65536, 64, 3), (131072, 32, 2), (65536, 8, 16), (65536, 4, 8), (65536, 2, 16), (65536, 16, 12),
-                                   (4, 16, 2048), (32, 2048, 16), (1, 512, 2), (1, 8192, 16), (256, 8192, 16)])
+                                   (4, 16, 2048), (32, 2048, 16), (1, 512, 2), (1, 8192, 16), (256, 8192, 16),
+                                   # split-K: few rows, long K
+                                   (1024, 32768, 64), (341, 4096, 64), (1, 65536, 32)])
 def test_skinny_and_few_row_steps(M, K, N, dtype):
     """Warp-cooperative skinny kernel (complex64, K <= 64, N <= 4) and the
     few-row kernel (Z*M < 4096) against the complex128 product of the same
