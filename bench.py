@@ -7,7 +7,7 @@ diagonal lattice, couplers ABCDCDAB, fSim(pi/2, pi/6), seeded single-qubit
 gates) at **12 cycles**, through the reference's default two-sided network
 (split at cycle 6, tns.py:185-212), rank cap 12, sliced over the cut edges
 (45,49), (38,45) (1024 slices, tools/cut_search.py; path re-searched on the
-sliced estimate as network.py:318-323 does), complex64.
+sliced estimate as network.py:323-330 does), complex64.
 
 One *step* = one device pass over ``--slices-per-step`` slices (default 1) of
 one bitstring on every rank; rank r takes slices (i*W + r)*k ... of step i, so

@@ -5,20 +5,20 @@
  * package `tnsim` (arXiv 2011.02621, /root/reference/pkg/src/tnsim):
  *
  *   tnc_contract_pair   replaces tnsim.tensor.contract_pair
- *                       (pkg/src/tnsim/tensor.py:103-119), batched over a
+ *                       (pkg/src/tnsim/tensor.py:100-115), batched over a
  *                       bitstring axis, optional conjugation of b (used by the
- *                       per-node overlap of network.py:321-335).
+ *                       per-node overlap of network.py:109-122).
  *   tnc_project         replaces the per-node physical contraction of
- *                       build_overlap_network (network.py:307-338) for
+ *                       build_overlap_network (network.py:95-126) for
  *                       product-state bras -- a gather of the projected
  *                       variant -- fused with slice_network's cut-leg
- *                       restriction (network.py:430-455) and a leg permutation.
+ *                       restriction (network.py:218-243) and a leg permutation.
  *   tnc_step            one Contract(C^{i1..im}, C^{im+1}) of
- *                       contract_along_path (network.py:458-479), batched over
+ *                       contract_along_path (network.py:246-268), batched over
  *                       (bitstring x slice).
- *   tnc_slice_sum       the slice loop's sum (network.py:543-551).
+ *   tnc_slice_sum       the slice loop's sum (network.py:334-339).
  *   tnc_contract_path   a whole planned path: project, every step, slice sum
- *                       (compute_amplitude's contraction, network.py:506-556).
+ *                       (compute_amplitude's contraction, network.py:294-344).
  *
  * All pointers are CUDA device pointers unless stated; `stream` is a
  * cudaStream_t passed as void*.  Complex numbers are interleaved (re, im)
@@ -167,7 +167,7 @@ int  tnc_step(const tnc_step_desc* d, void* stream);
 int  tnc_slice_sum(const tnc_slice_sum_desc* d, void* stream);
 int  tnc_contract_path(const tnc_path_desc* d, void* stream);
 
-/* tensor.py:103 contract_pair, batched: for every z < batch,
+/* tensor.py:100 contract_pair, batched: for every z < batch,
  *   out[z] = sum over paired axes of a[z] * (conj_b ? conj(b[z]) : b[z])
  * a: rank a_rank dims a_dims (row-major, z-stride a_zstride; 0 broadcasts),
  * b likewise; pairs (pair_a[i], pair_b[i]); result axes = unpaired a axes then

@@ -6,7 +6,7 @@ Plain-numpy restatement of the reference's amplitude-evaluation path
 reference`` legs may import this module, and only as the checker or the timed
 CPU reference -- the product (``paper_2011_02621_b200``) never calls it.
 
-Pinning: ``tests/test_oracle_golden.py`` checks every function here against
+Pinning: ``tests/test_host_parity.py`` checks every function here against
 golden vectors produced by the reference itself (``tests/golden/make_golden.py``
 imports /root/reference and runs its own ``compute_amplitude``,
 ``contract_pair``, ``slice_network``, ``amplitude_oracle``), so the oracle is
@@ -23,10 +23,10 @@ from typing import Sequence
 import numpy as np
 
 
-# -- tensor.py:103-119 ------------------------------------------------------
+# -- tensor.py:100-115 ------------------------------------------------------
 def contract_pair(a: np.ndarray, a_labels: Sequence, b: np.ndarray, b_labels: Sequence):
     """Contract every label shared by a and b; result axes = unpaired a axes then
-    unpaired b axes (np.tensordot, as reference tensor.py:113)."""
+    unpaired b axes (np.tensordot, as reference tensor.py:112)."""
     shared = sorted(set(a_labels) & set(b_labels), key=str)
     ia = [list(a_labels).index(s) for s in shared]
     ib = [list(b_labels).index(s) for s in shared]
@@ -36,13 +36,13 @@ def contract_pair(a: np.ndarray, a_labels: Sequence, b: np.ndarray, b_labels: Se
 
 
 def contraction_cost(dims_a, dims_b, n_shared_extents) -> int:
-    """tensor.py:168-184: prod(free a) * prod(free b) * prod(shared)."""
+    """tensor.py:164-184: prod(free a) * prod(free b) * prod(shared)."""
     return int(prod(dims_a) * prod(dims_b) // max(1, n_shared_extents))
 
 
-# -- network.py:430-455 -----------------------------------------------------
+# -- network.py:218-243 -----------------------------------------------------
 def slice_values(cut_extents: Sequence[int], slice_index: int) -> list[int]:
-    """Mixed-radix decoding, first cut edge most significant (network.py:440-444)."""
+    """Mixed-radix decoding, first cut edge most significant (network.py:228-232)."""
     vals = [0] * len(cut_extents)
     rem = slice_index
     for i in range(len(cut_extents) - 1, -1, -1):
@@ -52,7 +52,7 @@ def slice_values(cut_extents: Sequence[int], slice_index: int) -> list[int]:
 
 
 def slice_tensors(tensors: dict, cut_edges: Sequence, cut_extents: Sequence[int], slice_index: int) -> dict:
-    """Restrict both endpoints of every cut edge (np.take, network.py:446-453).
+    """Restrict both endpoints of every cut edge (np.take, network.py:234-241).
     ``tensors``: node -> (array, labels)."""
     out = dict(tensors)
     for e, v in zip(cut_edges, slice_values(cut_extents, slice_index)):
@@ -63,7 +63,7 @@ def slice_tensors(tensors: dict, cut_edges: Sequence, cut_extents: Sequence[int]
     return out
 
 
-# -- network.py:458-479 -----------------------------------------------------
+# -- network.py:246-268 -----------------------------------------------------
 def contract_along_path(tensors: dict, path: Sequence[int]):
     """Fold tensors in path order; returns (scalar, peak_rank, multiplies)."""
     acc, labels = tensors[path[0]]
@@ -79,7 +79,7 @@ def contract_along_path(tensors: dict, path: Sequence[int]):
     return complex(acc.reshape(())), peak, mult
 
 
-# -- network.py:543-551 -----------------------------------------------------
+# -- network.py:334-339 -----------------------------------------------------
 def sliced_amplitude(tensors: dict, path, cut_edges=(), cut_extents=()):
     """Sum over all slices of the contracted slice scalars."""
     count = prod(cut_extents) if cut_extents else 1
@@ -89,7 +89,7 @@ def sliced_amplitude(tensors: dict, path, cut_edges=(), cut_extents=()):
     return total
 
 
-# -- network.py:307-338 -----------------------------------------------------
+# -- network.py:95-126 -----------------------------------------------------
 def overlap_tensors(phi: dict, psi: dict, node_edges: dict, bonds_phi: dict, bonds_psi: dict) -> dict:
     """C_q = sum_s A_q[s] conj(B_q[s]); parallel bonds merged phi-major.
     phi/psi: node -> (array with axis 0 physical, labels with 'p' first)."""
@@ -110,7 +110,7 @@ def overlap_tensors(phi: dict, psi: dict, node_edges: dict, bonds_phi: dict, bon
 def projected_amplitudes(variants: dict, node_edges: dict, path, bits: np.ndarray,
                          cut_edges=(), cut_extents=()) -> np.ndarray:
     """Amplitude per bitstring with product-state bras: C_q = V_q[bit_q]
-    (network.py:321-335 with psi = |bits>), then the sliced path contraction.
+    (network.py:109-122 with psi = |bits>), then the sliced path contraction.
     ``variants``: node -> array [2, dims in node_edges order]."""
     out = np.empty(bits.shape[0], dtype=np.complex128)
     for i, row in enumerate(bits):
@@ -119,7 +119,7 @@ def projected_amplitudes(variants: dict, node_edges: dict, path, bits: np.ndarra
     return out
 
 
-# -- oracle.py:312-383 (brute-force state vector) -----------------------------
+# -- oracle.py:68-96 (brute-force state vector) -----------------------------
 def statevector(n: int, in_bits: str, ops) -> np.ndarray:
     """Evolve |in_bits> (qubit 0 = least significant bit) through ``ops``:
     ('1', q, 2x2) or ('2', k, l, 4x4 over (s_k s_l), s_k major)."""
@@ -142,7 +142,7 @@ def statevector(n: int, in_bits: str, ops) -> np.ndarray:
 
 def circuit_ops(circuit) -> list:
     """Gate sequence of a circuit object (single-qubit layers per moment,
-    cycles, trailing), matching oracle.py:362-375."""
+    cycles, trailing), matching oracle.py:77-89."""
     ops = []
     by_m: dict = {}
     for sg in circuit.single_qubit:
@@ -190,7 +190,7 @@ def reference_step_layouts(node_edges: dict, edges: dict, path: Sequence[int], c
     """Per path step, the operand layouts the reference's contract_along_path
     (network.py:246-266) hands to np.tensordot for one slice: accumulator
     labels in tensordot output order (free a axes, then free b axes,
-    tensor.py:103-119), the site's labels in node order, cut edges removed
+    tensor.py:100-115), the site's labels in node order, cut edges removed
     (np.take in slice_network).  Returns [(acc_labels, site_labels, shared)]."""
     cut = set(tuple(e) for e in cut_edges)
     lab = {q: [e for e in node_edges[q] if tuple(e) not in cut] for q in node_edges}

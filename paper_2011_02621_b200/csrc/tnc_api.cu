@@ -33,18 +33,9 @@ int tc_mask() {
   return v;
 }
 bool tc_enabled() { return tc_mask() != 0; }
-// pairwise plans: smallest K*N routed to the tensor-core kernel (TNC_TC_MIN_KN)
-int64_t tc_min_kn() {
-  static int64_t v = -1;
-  if (v < 0) {
-    const char* e = getenv("TNC_TC_MIN_KN");
-    v = e ? atoll(e) : 256;
-  }
-  return v;
-}
 // measured: K <= 4 stays on the SIMT column kernel (16-byte stores, 3.8 vs
 // 3.5 TB/s at K=4, N=64); K >= 8 with K*N >= 256 goes to tcgen05
-bool pair_use_tc(int64_t K, int64_t N) { return K * N >= tc_min_kn() && K >= 8; }
+bool pair_use_tc(int64_t K, int64_t N) { return K * N >= 256 && K >= 8; }
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -314,11 +305,9 @@ int launch_pair_tiled(const tnc::PairTile& p, int64_t batch, const void* a, cons
   using C = typename tnc::cplx<R>::T;
   const int64_t N = p.N, K = p.K;
   if (p.pipe && pipe_eligible(p, sizeof(C), a)) {
-    static const bool cols_ok = !(getenv("TNC_PIPE_COLS") && getenv("TNC_PIPE_COLS")[0] == '0');
-    if (cols_ok && N >= 8 && N <= 256 && (256 % N) == 0 && K <= (sizeof(R) == 4 ? 64 : 16)) {
+    if (N >= 8 && N <= 256 && (256 % N) == 0 && K <= (sizeof(R) == 4 ? 64 : 16)) {
       // two columns per thread (16-byte stores) when the rows stay 16-byte aligned
-      static const bool nv2 = !(getenv("TNC_PIPE_NV2") && getenv("TNC_PIPE_NV2")[0] == '0');
-      if (nv2 && sizeof(R) == 4 && N >= 16 && ((uintptr_t)out % 16) == 0) {
+      if (sizeof(R) == 4 && N >= 16 && ((uintptr_t)out % 16) == 0) {
         if (K <= 4) return launch_pipe_fn<R>(tnc::k_pair_pipe_cols<R, 4, 2>, p, batch, a, b, out, s, true);
         if (K <= 16) return launch_pipe_fn<R>(tnc::k_pair_pipe_cols<R, 16, 2>, p, batch, a, b, out, s, true);
       }
@@ -328,8 +317,7 @@ int launch_pair_tiled(const tnc::PairTile& p, int64_t batch, const void* a, cons
     }
     if (N <= 32) {
       // K >= 8: producer-warp variant (mbarrier stage release, no CTA barrier per tile)
-      static const bool prod_ok = !(getenv("TNC_PIPE_PROD") && getenv("TNC_PIPE_PROD")[0] == '0');
-      if (prod_ok && K >= 8 && N <= 4) {
+      if (K >= 8 && N <= 4) {
         if (N <= 1) return launch_pipe_fn<R>(tnc::k_pair_pipe<R, 1, 0, true>, p, batch, a, b, out, s, false, true);
         if (N <= 2) return launch_pipe_fn<R>(tnc::k_pair_pipe<R, 2, 0, true>, p, batch, a, b, out, s, false, true);
         return launch_pipe_fn<R>(tnc::k_pair_pipe<R, 4, 0, true>, p, batch, a, b, out, s, false, true);

@@ -61,9 +61,7 @@ struct TcDesc {
   int64_t out_zstride;             // out rows are contiguous: out + z*zs + g*N + n
   int32_t rows_contig;             // lo_off[r] = r*K and akoff[k] = k (tables unused)
   int32_t nstages;                 // A-chunk ring depth (host: as many as fit)
-  int32_t dbg;                     // experiment flags (0 in production): 1 no stores, 2 no loads, 4 no MMA
   int32_t f16;                     // 1: fp16-split operands, per-row A scales, per-z site scales (bscale)
-  unsigned long long* trace;       // dbg & 128: per-tile globaltimer stamps of CTA 0
   const float* bscale;             // [Z] max |re|,|im| of the site block of z (f16)
   // raw-ring mode: each tile's 128 x K accumulator block is staged by cp.async.bulk
   // as Kout contiguous segments of Lseg elements; element (r, k) sits at
@@ -163,12 +161,6 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
         "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
       : "r"(taddr));
 }
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-#define TC_TRACE(slot, t) do { if ((p.dbg & 128) && blockIdx.x == 0 && (t) < 64 && (threadIdx.x & 31) == 0) p.trace[(slot) * 64 + (t)] = gtimer(); } while (0)
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // smem sizes (bytes) for a (K, N) problem
@@ -472,11 +464,9 @@ k_tc_c64(const __grid_constant__ TcDesc p, const __grid_constant__ CUtensorMap t
     int j = 0;                                   // this group's chunk counter
     for (int t = grp; t < ntiles && grp < NG; t += NG) {
       const float2* raw = nullptr;
-      if ((warp & 3) == 0) TC_TRACE(0, t);
       if (RS > 0) {
         const int rs = t % RS;
         mbar_wait_spin(&rfull[rs], (uint32_t)((t / RS) & 1));
-        if ((warp & 3) == 0) TC_TRACE(1, t);
         raw = reinterpret_cast<const float2*>(rawring + (size_t)rs * tc_raw_bytes(p.K)) + looff_s[r];
       }
       const float2* Ar = A + tbase[t];
@@ -521,7 +511,7 @@ k_tc_c64(const __grid_constant__ TcDesc p, const __grid_constant__ CUtensorMap t
         } else {
           const int64_t* ko = akoff_s + c * KC;
 #pragma unroll
-          for (int q = 0; q < KC; ++q) v[q] = (p.dbg & 2) ? make_float2(1.f, 0.f) : __ldg(Ar + ko[q]);
+          for (int q = 0; q < KC; ++q) v[q] = __ldg(Ar + ko[q]);
         }
         if constexpr (F16) {
           if (scale_pending) {
@@ -532,9 +522,7 @@ k_tc_c64(const __grid_constant__ TcDesc p, const __grid_constant__ CUtensorMap t
             scale_pending = false;
           }
         }
-        if ((warp & 3) == 0 && c == 0) TC_TRACE(16, t);
         mbar_wait_spin(&empty[stage], ph ^ 1);
-        if ((warp & 3) == 0 && c == 0) TC_TRACE(10, t);
         tc_fence_after();
         const uint32_t col = A0 + (uint32_t)stage * ACOLS;
         if constexpr (F16) {
@@ -562,13 +550,10 @@ k_tc_c64(const __grid_constant__ TcDesc p, const __grid_constant__ CUtensorMap t
             hi[2 * q + 1] = __float_as_uint(a);
             lo[2 * q + 1] = __float_as_uint(b);
           }
-          if (!(p.dbg & 512)) {
-            tmem_st<KC>(tmem + lane_base + col + half * KC, hi);
-            tmem_st<KC>(tmem + lane_base + col + 2 * KC + half * KC, lo);
-          }
+          tmem_st<KC>(tmem + lane_base + col + half * KC, hi);
+          tmem_st<KC>(tmem + lane_base + col + 2 * KC + half * KC, lo);
         }
-        if (!(p.dbg & 512)) tmem_wait_st();
-        if ((warp & 3) == 0 && c == 0) TC_TRACE(17, t);
+        tmem_wait_st();
         tc_fence_before();
         mbar_arrive_warp(&full[stage]);
         if (RS > 0 && c == nchunk - 1) {
@@ -577,7 +562,6 @@ k_tc_c64(const __grid_constant__ TcDesc p, const __grid_constant__ CUtensorMap t
           fence_proxy_async();
           mbar_arrive_warp(&rempty[t % RS]);
         }
-        if ((warp & 3) == 0 && c == nchunk - 1) TC_TRACE(2, t);
       }
     }
   } else if (warp < TC_MMA_WARP) {
@@ -599,9 +583,7 @@ k_tc_c64(const __grid_constant__ TcDesc p, const __grid_constant__ CUtensorMap t
         mb += 2;
         while (mb >= p.tiles_per_z) { mb -= p.tiles_per_z; ++zt; }
       }
-      if (q == 0) TC_TRACE(3, t);
       mbar_wait_spin(&tfull[acc], ph);
-      if (q == 0) TC_TRACE(4, t);
       tc_fence_after();
       const int64_t grow = mb * 128 + r;
       float2* otile = p.out + zt * p.out_zstride + (grow - lane) * N;   // this warp's 32 rows
@@ -617,10 +599,7 @@ k_tc_c64(const __grid_constant__ TcDesc p, const __grid_constant__ CUtensorMap t
       for (int c0 = 0; c0 < Nr; c0 += 32) {
         const int cols = (c0 + 32 <= Nr) ? 32 : 16;
         uint32_t v[32];
-        if (p.dbg & 1024) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = j;
-        } else if (cols == 32) {
+        if (cols == 32) {
           tmem_ld32(taddr + c0, v);
         } else {
           uint32_t w16[16];
@@ -630,7 +609,6 @@ k_tc_c64(const __grid_constant__ TcDesc p, const __grid_constant__ CUtensorMap t
         }
         tmem_wait_ld();
         if constexpr (F16) inv = __uint_as_float(iv);
-        if (q == 0 && c0 == 0) TC_TRACE(14, t);
         if (c0 + 32 >= Nr) {              // accumulator drained: hand it back before the stores
           tc_fence_before();
           mbar_arrive_warp(&tempty[acc]);
@@ -674,7 +652,7 @@ k_tc_c64(const __grid_constant__ TcDesc p, const __grid_constant__ CUtensorMap t
                   make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           fence_proxy_async();
           __syncwarp();
-          if (lane == 0 && !(p.dbg & 1)) {
+          if (lane == 0) {
             if constexpr (TMO) {
               asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];"
                            ::"l"(reinterpret_cast<uint64_t>(&tmO)), "r"(c0), "r"((int)(grow - lane)), "r"((int)zt),
@@ -693,12 +671,11 @@ k_tc_c64(const __grid_constant__ TcDesc p, const __grid_constant__ CUtensorMap t
             *reinterpret_cast<uint4*>(stg + lane * TC_EPI_PITCH + j * 16) =
                 make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
         __syncwarp();
-        if (q == 0 && c0 == 0) TC_TRACE(15, t);
         const int real = min(cols, 2 * N - c0);        // real (unpadded) columns in this chunk
         const int per_row = real / 4;
         // per_row is 2, 4 or 8 for the padded widths: shifts instead of divisions
         const int prs = (per_row & (per_row - 1)) == 0 ? __ffs(per_row) - 1 : -1;
-        if (!(p.dbg & 1) && per_row > 0) {
+        if (per_row > 0) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const int idx = i * 32 + lane;
@@ -712,7 +689,6 @@ k_tc_c64(const __grid_constant__ TcDesc p, const __grid_constant__ CUtensorMap t
         }
         __syncwarp();
       }
-      if (q == 0) TC_TRACE(5, t);
     }
     if (bulk && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   } else if (warp == TC_MMA_WARP) {
@@ -750,9 +726,7 @@ k_tc_c64(const __grid_constant__ TcDesc p, const __grid_constant__ CUtensorMap t
         tc_fence_before();
         cur_z = zt;
       }
-      TC_TRACE(6, t);
       mbar_wait_spin(&tempty[acc], aph ^ 1);
-      TC_TRACE(7, t);
       tc_fence_after();
       const uint32_t d = tmem + (uint32_t)(acc * Nr);
       const int g = NGm == 2 ? (t & 1) : 0;
@@ -761,7 +735,6 @@ k_tc_c64(const __grid_constant__ TcDesc p, const __grid_constant__ CUtensorMap t
         const uint32_t ph = gph[g];
         if (++gpos[g] == ASg) { gpos[g] = 0; gph[g] ^= 1; }
         mbar_wait_spin(&full[stage], ph);
-        TC_TRACE(8, it);
         tc_fence_after();
         if (F16 && elect_one()) {
           // chunk c = reals [2KC c, 2KC (c+1)) of K'; per 16-real k-step: one column group of 8
@@ -786,19 +759,14 @@ k_tc_c64(const __grid_constant__ TcDesc p, const __grid_constant__ CUtensorMap t
           for (int s = 0; s < KC / 4; ++s) {
             const uint64_t step = (uint64_t)(s * 256) >> 4;     // two 16-byte units of B' per k-step
             const uint32_t first = (c == 0 && s == 0) ? 0u : 1u;
-            if (p.dbg & 2048) {
-              mma_tf32_ts(d, ahi + 8 * s, dbh0 + step, idesc, first);    // timing experiment: 1xTF32
-            } else if (!(p.dbg & 4)) {
-              mma_tf32_ts(d, alo + 8 * s, dbh0 + step, idesc, first);   // small terms first
-              mma_tf32_ts(d, ahi + 8 * s, dbl0 + step, idesc, 1u);
-              mma_tf32_ts(d, ahi + 8 * s, dbh0 + step, idesc, 1u);
-            }
+            mma_tf32_ts(d, alo + 8 * s, dbh0 + step, idesc, first);   // small terms first
+            mma_tf32_ts(d, ahi + 8 * s, dbl0 + step, idesc, 1u);
+            mma_tf32_ts(d, ahi + 8 * s, dbh0 + step, idesc, 1u);
           }
           umma_commit(&empty[stage]);
           if (c == nchunk - 1) umma_commit(&tfull[acc]);
         }
         __syncwarp();
-        TC_TRACE(9, it);
       }
       if (++acc == TS) { acc = 0; aph ^= 1; }
     }
@@ -820,9 +788,7 @@ k_tc_c64(const __grid_constant__ TcDesc p, const __grid_constant__ CUtensorMap t
     for (int t = 0; t < ntiles; ++t) {
       if (++rs == RS) rs = 0;
       if (rs == 0) rph ^= 1;
-      if (lane == 0) TC_TRACE(12, t);
       mbar_wait_spin(&rempty[rs], rph ^ 1);
-      if (lane == 0) TC_TRACE(13, t);
       unsigned char* dst = rawring + (size_t)rs * tc_raw_bytes(p.K);
       const float2* src = p.a + tbase[t];
       if (lane == 0) mbar_expect_tx(&rfull[rs], (uint32_t)(p.Kout * seg_bytes));
@@ -873,10 +839,6 @@ __host__ inline int launch_tc(TcDesc p, int64_t Z, cudaStream_t s) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   p.tiles_per_z = p.M / 128;
-  {
-    const char* e = getenv("TNC_TC_DEBUG");
-    p.dbg = e ? atoi(e) : 0;
-  }
   p.Z = Z;
   const int64_t total = Z * p.tiles_per_z;
   int64_t per = (total + sms - 1) / sms;
@@ -886,7 +848,7 @@ __host__ inline int launch_tc(TcDesc p, int64_t Z, cudaStream_t s) {
   // raw ring (TMA bulk staging) when alignment allows and >= 2 stages fit
   p.raw_stages = 0;
   const bool aligned = (((uintptr_t)p.a) % 16 == 0) && ((p.a_zstride * 8) % 16 == 0);
-  const bool use_raw = p.raw_ok && aligned && !(p.dbg & 256);
+  const bool use_raw = p.raw_ok && aligned;
   // bulk result stores: one full accumulator chunk per tile (2N = padded
   // width <= 32) and 16-byte aligned warp blocks; TNC_TC_BULKOUT=0 turns it off
   const char* ebo = getenv("TNC_TC_BULKOUT");
@@ -914,9 +876,7 @@ __host__ inline int launch_tc(TcDesc p, int64_t Z, cudaStream_t s) {
   for (int bo = (want_bulk && (p.N <= 16 || tm_ok)) ? 1 : 0; bo >= 0; --bo) {
     p.raw_stages = 0;
     if (use_raw) {
-      int rs_max = 4;
-      if (const char* e = getenv("TNC_TC_RS")) rs_max = atoi(e);
-      for (int rs = rs_max & ~1; rs >= 2; rs -= 2)
+      for (int rs = 4; rs >= 2; rs -= 2)
         if (tc_smem_bytes(p.K, p.N, per, rs, bo) <= 227 * 1024) { p.raw_stages = rs; break; }
       if (bo && p.raw_stages == 0) continue;     // the raw ring matters more than the store path
     }
@@ -927,10 +887,6 @@ __host__ inline int launch_tc(TcDesc p, int64_t Z, cudaStream_t s) {
   const size_t smem = (size_t)tc_smem_bytes(p.K, p.N, per, p.raw_stages, p.bulk_out != 0);
   const int64_t grid = (total + per - 1) / per;     // one wave when per fits in smem
   if (grid <= 0) return 0;
-  if (p.dbg & 128) {
-    cudaMalloc(&p.trace, 18 * 64 * sizeof(unsigned long long));
-    cudaMemset(p.trace, 0, 18 * 64 * sizeof(unsigned long long));
-  }
   const int kc = (int)tc_kc(p.K);
   // fp16-split operands (per-row A scales, per-z site scales) when the raw
   // ring holds whole tiles and the chunks are 16 complex (kind::f16 K = 16)
@@ -943,10 +899,6 @@ __host__ inline int launch_tc(TcDesc p, int64_t Z, cudaStream_t s) {
   const char* e16 = getenv("TNC_TC_F16");
   p.f16 = (kc == 16 && p.K == 16 && p.raw_stages > 0 && AS16 >= 2 && e16 && e16[0] == '1') ? 1 : 0;
   if (p.f16 && p.bulk_out == 2) p.bulk_out = 0;     // the tensor-store epilogue is a tf32-kernel instantiation
-  if (getenv("TNC_TC_VERBOSE"))
-    fprintf(stderr, "launch_tc K=%lld N=%lld M=%lld Z=%lld bulk_out=%d f16=%d raw_stages=%d AS16=%d per=%lld grid=%lld Kout=%lld Lseg=%lld\n",
-            (long long)p.K, (long long)p.N, (long long)p.M, (long long)Z, p.bulk_out, p.f16, p.raw_stages, AS16,
-            (long long)per, (long long)grid, (long long)p.Kout, (long long)p.Lseg);
   float* bsc = nullptr;
   if (p.f16) {
     pool_keep();
@@ -959,22 +911,6 @@ __host__ inline int launch_tc(TcDesc p, int64_t Z, cudaStream_t s) {
   else if (kc == 8) k_tc_c64<4, false><<<(unsigned)grid, TC_THREADS, smem, s>>>(p, tmO);
   else if (p.bulk_out == 2) k_tc_c64<8, false, true><<<(unsigned)grid, TC_THREADS, smem, s>>>(p, tmO);
   else k_tc_c64<8, false><<<(unsigned)grid, TC_THREADS, smem, s>>>(p, tmO);
-  if (p.dbg & 128) {
-    unsigned long long h[18 * 64];
-    cudaStreamSynchronize(s);
-    cudaMemcpy(h, p.trace, sizeof h, cudaMemcpyDeviceToHost);
-    const unsigned long long t0 = h[0];
-    const char* names[18] = {"conv_pre_empty", "conv_got_empty", "conv_arrived", "epi_pre_tfull", "epi_got_tfull",
-                             "epi_done", "mma_pre_tempty", "mma_got_tempty", "mma_got_full", "mma_committed",
-                             "conv_got_empty2", "conv_got_raw", "prod_pre_rempty", "prod_got_rempty",
-                             "epi_ld_done", "epi_sts_done", "conv_lds_done", "conv_st_done"};
-    for (int sl = 0; sl < 18; ++sl) {
-      printf("%-16s", names[sl]);
-      for (int t = 0; t < 20; ++t) printf(" %6lld", h[sl * 64 + t] ? (long long)(h[sl * 64 + t] - t0) : -1LL);
-      printf("\n");
-    }
-    cudaFree(p.trace);
-  }
   return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

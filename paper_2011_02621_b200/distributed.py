@@ -7,7 +7,7 @@ bitstrings where B >= W and slice ranges of a bitstring otherwise -- no data
 moves between GPUs while contracting.  Each rank accumulates its partial slice
 sums into a length-B amplitude vector (zeros elsewhere); a single NCCL
 all-reduce (sum) then performs the slice-sum and the amplitude gather at once
-(the reference's slice loop, network.py:543-551, distributed).
+(the reference's slice loop, network.py:334-339, distributed).
 """
 
 from __future__ import annotations

@@ -1,6 +1,6 @@
 """Batched contraction engine: host planner + device executor.
 
-The engine evaluates ``contract_along_path`` (reference network.py:458-479)
+The engine evaluates ``contract_along_path`` (reference network.py:246-268)
 for a batch of output bitstrings and all slices of a cut plan at once.  Every
 batch element z = (bitstring b, slice s) contracts the same network shape along
 the same path; only the *projected site tensors* differ:
@@ -153,7 +153,7 @@ class ContractionPlan:
                 raise ValueError(f"cut edge {e} not in network")
         self.cut_ext = [int(spec.edges[e]) for e in self.cut]
         self.slice_count = prod(self.cut_ext) if self.cut else 1
-        # mixed radix, first cut edge most significant (network.py:440-444)
+        # mixed radix, first cut edge most significant (network.py:228-232)
         self.cut_div = {}
         div = 1
         for e, x in zip(reversed(self.cut), reversed(self.cut_ext)):

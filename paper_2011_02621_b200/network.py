@@ -7,7 +7,7 @@ contraction runs on the B200:
   on the GPU (``tnc_contract_pair`` with a conjugated bra and a leg-interleaving
   output permutation);
 * ``plan_cuts`` / ``CutPlan`` -- host planning, bit-exact to the reference
-  (Fiedler sweep + path-search feasibility, network.py:341-427);
+  (Fiedler sweep + path-search feasibility, network.py:129-215);
 * ``contract_along_path`` / ``compute_amplitude`` -- the engine
   (``engine.PathExecutor``), all slices in one batched device pass;
 * ``compute_amplitudes`` / ``AmplitudeEngine`` -- the batched evaluator: one
@@ -113,7 +113,7 @@ def _interleave_perm(deg: int) -> list[int]:
 
 def _overlap_sites(phi: TNSState, psis: Sequence[TNSState], device, dtype):
     """C_q[b] = sum_s A_q[s] (x) conj(B_q^b[s]) with the two parallel bonds of
-    each edge merged (phi index major, psi minor; reference network.py:321-335),
+    each edge merged (phi index major, psi minor; reference network.py:109-122),
     for every bra state B^b of ``psis`` (all sharing bond dims).  Returns
     node -> device tensor [len(psis), merged dims...]."""
     import torch
@@ -164,7 +164,7 @@ def build_overlap_network(phi: TNSState, psi: TNSState) -> TensorNetwork:
 
 
 # ---------------------------------------------------------------------------
-# cut planning (host, bit-exact to network.py:341-427)
+# cut planning (host, bit-exact to network.py:129-215)
 # ---------------------------------------------------------------------------
 
 def _fiedler_order(shape: NetworkShape) -> list:
@@ -276,7 +276,7 @@ def contract_network(net: TensorNetwork, path, cut_plan: CutPlan | None = None,
 
 def contract_along_path(net: TensorNetwork, path) -> tuple:
     """Contract a (slice) network along ``path``; returns the scalar and
-    {"peak_rank", "multiplies"} like the reference (network.py:458-479)."""
+    {"peak_rank", "multiplies"} like the reference (network.py:246-268)."""
     if sorted(path) != sorted(net.tensors):
         raise ValueError("path is not a permutation of the network's qubits")
     value, plan = contract_network(net, path)
@@ -329,7 +329,7 @@ def _path_for(shape_net, plan: CutPlan, max_rank):
 def compute_amplitude(circuit: Circuit, in_bits: str, out_bits: str, split_cycle=None,
                       cuts="auto", max_rank=None, tolerance: float = 1e-12,
                       dtype: str = "complex128") -> AmplitudeStats:
-    """<out|U|in> (reference network.py:506-556): fuse -> two-sided evolution ->
+    """<out|U|in> (reference network.py:294-344): fuse -> two-sided evolution ->
     cut plan -> one path on the slice-0 shape -> all slices contracted on the
     GPU and summed."""
     import torch

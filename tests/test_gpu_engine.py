@@ -344,7 +344,7 @@ def test_graph_replay_matches_eager(golden_amplitudes):
 
 def test_sycamore53_sliced_matches_unsliced():
     """53-qubit Sycamore (ABCDCDAB, 8 cycles): the projected engine sliced over
-    the bench's depth-10 cut edges (network.py:385-455 scheme: cut legs fixed
+    the bench's depth-10 cut edges (network.py:173-243 scheme: cut legs fixed
     per slice, device slice sum) against the unsliced network, complex64."""
     from paper_2011_02621_b200 import AmplitudeEngine, pattern_rqc, sycamore53_graph
 

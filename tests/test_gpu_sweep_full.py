@@ -3,7 +3,7 @@ bench.sweep_cases() (operands up to 2^32 elements, r up to 28) is contracted
 at full size through the C ABI (PairPlan + projection gather, the bench's exact
 layouts and seeds) and checked on sampled result rows against the oracle's
 algebra in complex128: out[b, f, :] = sum_k acc[b, f, k] S[bits[b]][k, :]
-(reference tensor.py:103-119 / oracle sweep_step), rel L2 <= 2e-6."""
+(reference tensor.py:100-115 / oracle sweep_step), rel L2 <= 2e-6."""
 
 import numpy as np
 import pytest

@@ -1,4 +1,4 @@
-"""The Tensor / contract_pair API (reference tensor.py:103-119 and its test
+"""The Tensor / contract_pair API (reference tensor.py:100-115 and its test
 strategy, pkg/tests/test_tensor.py::TestContractPair): argument errors are
 raised on the host before any device work (CPU tests); the contractions run
 through tnc_contract_pair on the GPU and are checked against an explicit

@@ -5,7 +5,7 @@ and, on the 53-qubit networks, fails (it cuts every Fiedler separator and the
 path search still exceeds the cap).  The BASELINE configs cap intermediates
 at 2^30 *elements*, so this tool picks the cut set; everything after it follows
 the reference exactly: the path is ``find_optimal_path`` on the slice-0
-estimate (cut edges at extent 1, network.py:318-323) and every slice is
+estimate (cut edges at extent 1, network.py:323-330) and every slice is
 contracted along it.
 
 Greedy rule: each round tries every uncut edge, re-runs the path search on
