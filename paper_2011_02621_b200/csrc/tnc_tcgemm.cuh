@@ -67,6 +67,7 @@ struct GemmDesc {
   int32_t nf, c_rows_contig;
   int64_t f_dim[TNC_MAX_LEGS], f_cstride[TNC_MAX_LEGS];
   const int64_t* c_noff;         // [N]
+  unsigned int* progress;        // pair kernel: items whose A loads have been issued, summed over CTAs (zeroed by the host)
 };
 
 // warps: converters [0, CONVW), epilogue [CONVW, MMA), MMA issuer, A and B producers;
@@ -117,6 +118,29 @@ __device__ __forceinline__ void split_f16x2(float y0, float y1, uint32_t& h, uin
   const float l0 = y0 - h0, l1 = y1 - h1;
   asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(h1), "f"(h0));
   asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(l) : "f"(l1), "f"(l0));
+}
+
+// Two values -> packed fp16 hi and lo (low half = y0): hi by one packed
+// conversion, converted back (one HADD2.F32 each) for lo = y - hi, which is
+// exact in fp32 (6 instructions per pair; split_f16x2's integer rounding takes 8)
+__device__ __forceinline__ void split_f16x2_cvt(float y0, float y1, uint32_t& h, uint32_t& l) {
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(y1), "f"(y0));
+  const __half2 hh = *reinterpret_cast<const __half2*>(&h);
+  const float l0 = y0 - __low2float(hh), l1 = y1 - __high2float(hh);
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(l) : "f"(l1), "f"(l0));
+}
+
+// wait of a mostly idle role (epilogue on tfull): the hardware may suspend the
+// thread for up to ~4 us per try_wait, so the poll loop takes no issue slots
+// from the converter warps of its SM sub-partition
+__device__ __forceinline__ void mbar_wait_idle(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}" ::"r"(smem_u32(bar)), "r"(phase), "r"(4000u) : "memory");
 }
 
 // per combo (blockIdx.x): max |re|, |im| over the site block (F16 scale of
@@ -359,9 +383,10 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
             const uint32_t phys = off ^ (((off >> 7) & SWM) << 4);
             float4 x;
             asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w) : "r"(src + phys));
-            split_f16x2(x.x * sA, x.z * sA, rh[q], rl[q]);
-            split_f16x2(x.y * sA, x.w * sA, ih[q], il[q]);
-            split_f16x2((x.x + x.y) * sA, (x.z + x.w) * sA, sh[q], sl[q]);
+            const float r0 = x.x * sA, i0 = x.y * sA, r1 = x.z * sA, i1 = x.w * sA;
+            split_f16x2_cvt(r0, r1, rh[q], rl[q]);
+            split_f16x2_cvt(i0, i1, ih[q], il[q]);
+            split_f16x2_cvt(r0 + i0, r1 + i1, sh[q], sl[q]);
           }
           mbar_wait_spin(&aempty[astage], aph ^ 1);
           tc_fence_after();
@@ -492,7 +517,8 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
           inv2 = 1.f / op_scale(__ldg(p.bscale + gemm_combo(p, z)), G3);
         }
       }
-      mbar_wait(&tfull[acc], ph);
+      if constexpr (G3) mbar_wait_idle(&tfull[acc], ph);
+      else mbar_wait(&tfull[acc], ph);
       tc_fence_after();
       const uint32_t tre = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * NACC * NT);
       if (cfirst >= NT) {                         // no columns for this group
@@ -733,6 +759,10 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
   }
 }
 
+}  // namespace tnc
+#include "tnc_tcgemm2.cuh"
+namespace tnc {
+
 __host__ inline size_t tg_smem_bytes(int NT, int KC, int RS, int BS, int f16, int64_t cn = 0) {
   return 1024 + (size_t)RS * 128 * KC * 8 + (size_t)BS * 6 * tg_block_bytes(NT, KC, f16) +
          (size_t)(f16 ? 8 : 4) * 32 * TG_EPI_PITCH +
@@ -838,22 +868,36 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return 0;
     p.bp_combo_stride = (int64_t)p.tiles_n * p.nchunk * 6 * tg_block_bytes(p.NT, KC, f16);
+    const bool pair = tg2_applicable(p);
+    if (pair) {
+      // pair kernel: 96 KB result stage, 12 KB B' half stages
+      p.cn_smem = (!d.c_rows_contig && d.N <= 2048 && d.out_zstride < 0x7fffffffLL) ? 1 : 0;
+      const int64_t cn2 = p.cn_smem ? d.N : 0;
+      RS = 3; BS = 3;
+      while (RS + 1 <= TG2_MAX_RS && RS < 5 && tg2_smem_bytes(RS + 1, BS, cn2) <= budget) ++RS;
+      while (BS + 1 <= TG2_MAX_BS && tg2_smem_bytes(RS, BS + 1, cn2) <= budget) ++BS;
+      while (RS + 1 <= TG2_MAX_RS && tg2_smem_bytes(RS + 1, BS, cn2) <= budget) ++RS;
+      if (tg2_smem_bytes(RS, BS, cn2) > budget) return 0;
+      p.RS = RS; p.BS = BS;
+    }
     unsigned char* bp = nullptr;
     pool_keep();
     // one allocation: B' blocks, then (F16) the per-combo site maxima
     const size_t bp_bytes = ((size_t)combos * p.bp_combo_stride + 255) & ~(size_t)255;
-    if (cudaMallocAsync(reinterpret_cast<void**>(&bp), bp_bytes + (f16 ? combos * 4 : 0), s) != cudaSuccess) return -1;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&bp), bp_bytes + (f16 ? combos * 4 + 16 : 0), s) != cudaSuccess) return -1;
     p.bp = bp;
     {
       const int64_t work = combos * p.tiles_n * p.nchunk * p.NT * KC;
       int blocks = (int)std::min<int64_t>((work + 255) / 256, 148 * 16);
       if (f16) {
         float* bsc = reinterpret_cast<float*>(bp + bp_bytes);
-        if (cudaMemsetAsync(bsc, 0, combos * 4, s) != cudaSuccess) return -1;
+        if (cudaMemsetAsync(bsc, 0, combos * 4 + 16, s) != cudaSuccess) return -1;
+        p.progress = reinterpret_cast<unsigned int*>(bsc + combos);
         const unsigned ky = (unsigned)std::min<int64_t>(d.K, std::max<int64_t>(1, 296 / combos));
         k_bscale<<<dim3((unsigned)combos, ky), d.N >= 256 ? 256 : 128, 0, s>>>(p, bsc);
         p.bscale = bsc;
-        k_bprime<true><<<blocks < 1 ? 1 : blocks, 256, 0, s>>>(p, combos);
+        if (pair) k_bprime_pair<<<blocks < 1 ? 1 : blocks, 256, 0, s>>>(p, combos);
+        else k_bprime<true><<<blocks < 1 ? 1 : blocks, 256, 0, s>>>(p, combos);
       } else {
         k_bprime<false><<<blocks < 1 ? 1 : blocks, 256, 0, s>>>(p, combos);
       }
@@ -878,7 +922,30 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
       cudaFuncSetAttribute(k_tc_gemm<16, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       attr |= 1ull << (adev & 63);
     }
-    if (p.g3) k_tc_gemm<16, true, true><<<(unsigned)grid, TG_THREADS_G3, smem, s>>>(p, tm);
+    if (pair) {
+      // B' as rows of 1 KB: one 12-row box per half chunk
+      CUtensorMap tmb;
+      const cuuint64_t bdim[2] = {256u, (cuuint64_t)((combos * p.bp_combo_stride) >> 10)};
+      const cuuint64_t bstr[1] = {1024u};
+      const cuuint32_t bbox[2] = {256u, 12u};
+      const cuuint32_t bes[2] = {1u, 1u};
+      if (enc(&tmb, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, bp, bdim, bstr, bbox, bes, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+        cudaFreeAsync(bp, s);
+        return -1;
+      }
+      static uint64_t attr2 = 0;
+      int adev2 = 0;
+      if (attr_needed(attr2, &adev2)) {
+        cudaFuncSetAttribute(k_tc_gemm2, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr2 |= 1ull << (adev2 & 63);
+      }
+      const int64_t W = p.Z * ((p.tiles_m + 1) / 2) * p.tiles_n;
+      const int64_t npairs = std::min<int64_t>(sms / 2, W);
+      const size_t smem2 = tg2_smem_bytes(p.RS, p.BS, p.cn_smem ? d.N : 0);
+      k_tc_gemm2<<<(unsigned)(2 * npairs), TG2_THREADS, smem2, s>>>(p, tm, tmb);
+    } else if (p.g3) k_tc_gemm<16, true, true><<<(unsigned)grid, TG_THREADS_G3, smem, s>>>(p, tm);
     else if (f16) k_tc_gemm<16, true><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm);
     else if (KC == 16) k_tc_gemm<16, false><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm);
     else k_tc_gemm<8, false><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm);

@@ -213,7 +213,11 @@ def test_tc_gemm_scaled_precision(M, K, N):
                                                  # 128-wide 3M (Gauss) tiles, K > 128; round-robin item order
                                                  (8192, 256, 256, 1.0, 1.0), (4096, 512, 128, 3e-21, 1.0),
                                                  (2048, 1024, 384, 1e-25, 1e-12), (4096, 256, 200, 7e12, 1.0),
-                                                 (1536, 2048, 1024, 1.0, 1e-3)])
+                                                 (1536, 2048, 1024, 1.0, 1e-3),
+                                                 # CTA-pair kernel (K >= 512): odd row-tile count (last pair half
+                                                 # empty), ragged N, rows past M
+                                                 (3200, 512, 384, 1.0, 1.0), (3100, 1024, 200, 3e-21, 1e-3),
+                                                 (8192, 512, 128, 7e12, 1.0)])
 def test_tc_gemm_f16_split_step(M, K, N, scale, sscale):
     """fp16-split tcgen05 GEMM (a step given amax_in): one step acc[M, K] x
     S[K, N] on inputs spanning ~12 decades around an arbitrary overall scale
