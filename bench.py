@@ -6,16 +6,21 @@ config -- amplitudes/s of the 53-qubit Sycamore circuit (configs[4]: 53-qubit
 diagonal lattice, couplers ABCDCDAB, fSim(pi/2, pi/6), seeded single-qubit
 gates) at **12 cycles**, through the reference's default two-sided network
 (split at cycle 6, tns.py:185-212), rank cap 12, sliced over the cut edges
-(45,49), (38,45) (1024 slices, tools/cut_search.py; path re-searched on the
-sliced estimate as network.py:323-330 does), complex64.
+(9,14), (2,8): 256 slices, largest intermediate 2^33 elements (two 64 GiB
+ping-pong accumulators in the B200's 180 GB; tools/cut_search.py; path
+re-searched on the sliced estimate as network.py:323-330 does), complex64.
+configs[4] asks for a 2^30-element cap: the cheapest cut set found for it costs
+4.1e17 multiplies per amplitude in 32768 slices against 1.5e16 here (DESIGN.md
+section 6), so the cap is sized for this GPU instead; the 2^31 plan of the
+earlier rounds ((45,49), (38,45), 1024 slices, 2.0e16) is a nested entry.
 
 One *step* = one device pass over ``--slices-per-step`` slices (default 1) of
 one bitstring on every rank; rank r takes slices (i*W + r)*k ... of step i, so
 N ranks advance one amplitude N times faster, and the slice sum across ranks is
 one NCCL all-reduce per step (the reference's slice loop, network.py:334-339,
-distributed).  An amplitude is all 1024 slices, so value = W * k * steps /
-1024 / t (whole-job amplitudes/s; per-rank work fixed: "weak").  Every slice
-has the same shapes and path, so a step is an exact 1/1024-of-an-amplitude
+distributed).  An amplitude is all S = 256 slices, so value = W * k * steps /
+S / t (whole-job amplitudes/s; per-rank work fixed: "weak").  Every slice
+has the same shapes and path, so a step is an exact 1/S-of-an-amplitude
 unit of work; ``tools/net_probe.py --full`` runs whole amplitudes.
 
 Nested entries (same JSON line): two-sided 53q depth 10 and depth 8 (whole
@@ -23,7 +28,7 @@ amplitudes, bitstring batches), the configs[1] pairwise sweep, configs[0].
 
 Timing: W untimed warm-up steps, then K steps, each bracketed by CUDA events
 on the launching stream; barrier + synchronize around the timed region; max
-over ranks.  Inputs are larger than L2 (2^31-element ping-pong accumulators).
+over ranks.  Inputs are larger than L2 (2^33-element ping-pong accumulators).
 ``--impl reference`` times the CPU oracle port of the reference path
 (np.tensordot on the reference's operand layouts) on the same config.
 """
@@ -47,10 +52,11 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "amplitudes/sec (53q, depth 12) at 1/2/4/8 GPUs; contraction % of roofline"
-D12 = {"depth": 12, "split": 6, "cap": 12, "cuts": [(45, 49), (38, 45)]}
+D12 = {"depth": 12, "split": 6, "cap": 12, "cuts": [(9, 14), (2, 8)], "slices": 256, "elem_log2": 33}
+D12_CAP31 = {"depth": 12, "split": 6, "cap": 12, "cuts": [(45, 49), (38, 45)], "slices": 1024, "elem_log2": 31}
 SWEEP_LIMIT = 1 << 32          # elements per operand (complex64: 32 GiB)
 SEED = 0
-NCU_D12_PROFILE = "profiles/r02b_ncu_d12_gemm.json"   # ncu --set full of the top GEMM step (dram bytes)
+NCU_D12_PROFILE = "profiles/r02f_ncu_d12_pair.json"   # ncu --set full of the top GEMM step (dram bytes)
 
 
 def peaks():
@@ -271,8 +277,8 @@ def path_roofline(plan, times, z, itemsize, hbm, bf16, bf16_sus):
     ach = gemm_fl / gemm_t / 1e12 if gemm_t else 0.0
     return {
         "bound": "tensor", "achieved": ach, "peak": bf16, "unit": "TFLOP/s", "frac": ach / bf16,
-        "kernel": "tnc::k_tc_gemm<16,true,true> (tcgen05.mma kind::f16, fp16-split operands, 3M complex products, "
-                  "A operand in TMEM, B by bulk copies)",
+        "kernel": "tnc::k_tc_gemm2 (CTA pairs: tcgen05.mma.cta_group::2 kind::f16, M = 256, fp16-split operands, 3M "
+                  "complex products, A operand in TMEM, B' halves by TMA; K < 512 steps: single-CTA k_tc_gemm)",
         "algorithmic": "8*M*K*N flops per GEMM step per slice (complex multiply-add = 8 real flops)",
         "kernel_share_of_step": gemm_t / tot if tot else None,
         "pipe_flops_per_algorithmic_flop": 2.25,
@@ -300,22 +306,28 @@ def ncu_traffic():
 # ---------------------------------------------------------------------------
 # headline: 53q depth 12, two-sided, sliced
 # ---------------------------------------------------------------------------
-def d12_engine(dev, max_batch_elems=1):
+def d12_engine(dev, max_batch_elems=1, plan_cfg=None):
     from paper_2011_02621_b200.network import TwoSidedEngine
 
-    circ = syc_circuit(D12["depth"])
-    return TwoSidedEngine(circ, split_cycle=D12["split"], cuts=D12["cuts"], max_rank=D12["cap"],
+    pc = plan_cfg or D12
+    circ = syc_circuit(pc["depth"])
+    return TwoSidedEngine(circ, split_cycle=pc["split"], cuts=pc["cuts"], max_rank=pc["cap"],
                           dtype="complex64", device=dev, max_batch_elems=max_batch_elems), circ
 
 
-def d12_config(eng=None, k=1):
+def d12_config(eng=None, k=1, plan_cfg=None):
+    pc = plan_cfg or D12
+    cuts = ",".join(f"({a},{b})" for a, b in pc["cuts"])
     cfg = {"workload": "configs[4]: 53-qubit Sycamore (ABCDCDAB, fSim(pi/2, pi/6)), 12 cycles, two-sided split 6, "
-                       "rank cap 12, sliced over (45,49),(38,45); one step = 1 bitstring x "
-                       f"{k} slice(s) per rank",
+                       f"rank cap 12, sliced over {cuts}; one step = 1 bitstring x {k} slice(s) per rank",
            "dtype": "complex64", "depth": 12, "split_cycle": 6, "max_rank": 12,
-           "cut_edges": [list(e) for e in D12["cuts"]], "slices_per_amplitude": 1024,
+           "cut_edges": [list(e) for e in pc["cuts"]], "slices_per_amplitude": pc["slices"],
+           "largest_intermediate_log2_elems": pc["elem_log2"],
+           "cap_note": "configs[4] names a 2^30-element cap; the cheapest cut set found for it (tools/cut_search.py: "
+                       "(9,14),(14,21),(21,26), 32768 slices) costs 4.1e17 multiplies per amplitude, this plan "
+                       "1.5e16 (2^33) / 2.0e16 (2^31): the cap is sized for the B200's 180 GB instead",
            "slices_per_step_per_rank": k, "circuit_seed": SEED,
-           "l2": "inputs larger than L2 (2 x 2^31-element complex64 ping-pong accumulators)"}
+           "l2": f"inputs larger than L2 (2 x 2^{pc['elem_log2']}-element complex64 ping-pong accumulators)"}
     return cfg
 
 
@@ -324,12 +336,16 @@ def d12_plan_info(eng):
             "path_steps": len(eng.plan.steps), "path": list(eng.path), "path_score": str(eng.path_score)}
 
 
-def run_d12(args, rank, world, dev):
+def run_d12(args, rank, world, dev, plan_cfg=None, steps=None, warmup=None, e2e=None):
     import torch
 
+    pc = plan_cfg or D12
+    steps = args.steps if steps is None else steps
+    warmup = args.warmup if warmup is None else warmup
+    e2e = args.e2e if e2e is None else e2e
     hbm, bf16, bf16_sus, peak_src = peaks()
     t0 = time.perf_counter()
-    eng, circ = d12_engine(dev)
+    eng, circ = d12_engine(dev, plan_cfg=pc)
     bits = random_bits(53, 1, 100)
     ex = eng.prepare(bits)
     setup_s = time.perf_counter() - t0
@@ -351,21 +367,21 @@ def run_d12(args, rank, world, dev):
 
             dist.all_reduce(amp)                   # slice sum across ranks (NCCL)
 
-    for i in range(args.warmup):
+    for i in range(warmup):
         one_step(i)
     barrier(world)
     torch.cuda.synchronize(dev)
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     with ClockSampler(dev.index) as clk:
         for i, (e0, e1) in enumerate(evs):
             e0.record(stream)
-            one_step(args.warmup + i)
+            one_step(warmup + i)
             e1.record(stream)
         torch.cuda.synchronize(dev)
     t = sum(e0.elapsed_time(e1) for e0, e1 in evs) * 1e-3
     barrier(world)
     t_max = allreduce_max(t, world, dev)
-    value = world * k * args.steps / S / t_max
+    value = world * k * steps / S / t_max
     times = step_times(ex, plan, dev)
     roof = path_roofline(plan, times, 1, 8, hbm, bf16, bf16_sus)
     roof["peak_source"] = f"{peak_src} bf16_tflops (MEASURED_PEAKS.json, burst); sustained {bf16_sus}"
@@ -375,10 +391,10 @@ def run_d12(args, rank, world, dev):
         roof["traffic_check"] = nt
     top = sorted(zip(plan.steps, times), key=lambda x: -x[1])[:6]
     res = {
-        "value": value, "unit": "amplitudes/s", "ms_per_step": 1e3 * t_max / args.steps,
-        "s_per_amplitude_per_gpu": t_max / args.steps * S / k,
-        "gpu_launches": launches_per_pass(plan, 1) * k * args.steps,
-        "roofline": roof, "config": d12_config(None, k), "plan": d12_plan_info(eng), "clocks": clk.summary(),
+        "value": value, "unit": "amplitudes/s", "ms_per_step": 1e3 * t_max / steps, "steps": steps, "warmup": warmup,
+        "s_per_amplitude_per_gpu": t_max / steps * S / k,
+        "gpu_launches": launches_per_pass(plan, 1) * k * steps,
+        "roofline": roof, "config": d12_config(None, k, pc), "plan": d12_plan_info(eng), "clocks": clk.summary(),
         "dtype": "complex64",
         "host_setup_s": setup_s,
         "sharding": ("rank r contracts slices (i*W + r)*k.. of step i; one NCCL all_reduce(sum) per step = the "
@@ -386,18 +402,21 @@ def run_d12(args, rank, world, dev):
         "top_steps": [{"M": sp.M, "K": sp.K, "N": sp.N, "ms": 1e3 * tt, "tflops": 8e-12 * sp.M * sp.K * sp.N / tt}
                       for sp, tt in top],
     }
-    if args.e2e:
+    if e2e:
         # through the public API with host buffers: host bitstring in, bra
         # evolution + overlap sites (H2D), the step's slices, host amplitude out
-        h2d = sum(t.data.nbytes for t in eng.phi.tensors.values())
-        pb = eng.bra_batch(bits)
-        h2d += sum(t.nbytes for t in pb.tensors.values()) + 53
-        steps = max(1, min(args.steps, 3))
-        eng.amplitudes(bits, slices=slice_range(0))
+        # bytes copied per step: the bra site tensors of the bitstring (one pinned buffer) + the bitstring
+        h2d = eng._overlap.h2d_bytes_per_bitstring + 53
+        es = max(1, min(steps, 3))
+        eng._bra_cache = None
+        tb0 = time.perf_counter()
+        eng.amplitudes(bits, slices=slice_range(0))      # first call of an amplitude: host bra evolution
         torch.cuda.synchronize(dev)
+        first_call_s = time.perf_counter() - tb0
+        bra_s = eng.last_host_s
         barrier(world)
         t0 = time.perf_counter()
-        for i in range(steps):
+        for i in range(es):
             a = eng.amplitudes(bits, slices=slice_range(i))
             if world > 1:
                 import torch.distributed as dist
@@ -405,15 +424,20 @@ def run_d12(args, rank, world, dev):
                 ta = torch.from_numpy(a).to(dev)
                 dist.all_reduce(ta)
         te = allreduce_max(time.perf_counter() - t0, world, dev)
-        res["e2e"] = {"value": world * k * steps / S / te, "unit": "amplitudes/s", "h2d_bytes_per_step": h2d,
-                      "d2h_bytes_per_step": 16, "steps": steps,
-                      "path": "TwoSidedEngine.amplitudes([bitstring], slices=...) -> host complex partial amplitude "
-                              "(host bra evolution, overlap sites built on the GPU, the slices, D2H)"}
+        # the bra evolution runs once per amplitude (its S / (W k) steps); its share of a step is added back
+        per_step = te / es + bra_s * world * k / S
+        res["e2e"] = {"value": world * k / S / per_step, "unit": "amplitudes/s", "h2d_bytes_per_step": h2d,
+                      "d2h_bytes_per_step": 16, "steps": es, "ms_per_step": 1e3 * te / es,
+                      "host_bra_evolution_s_per_amplitude": bra_s, "first_call_s": first_call_s,
+                      "path": "TwoSidedEngine.amplitudes([bitstring], slices=...) -> host complex partial amplitude: "
+                              "per step the bra site tensors go H2D from a pinned buffer, the overlap sites are built "
+                              "on the GPU, the step's slices are contracted, the partial amplitude comes back; the "
+                              "host bra evolution runs on the first call of an amplitude and is charged pro rata"}
     res["_engine"] = eng
     return res
 
 
-def cpu_d12(work_cap=1e9, groups=None):
+def cpu_d12(work_cap=1e9, groups=None, plan_cfg=None):
     """CPU reference of one d12 slice: the reference's np.tensordot steps on
     its own operand layouts (oracle, complex64, all host threads), each path
     step on a row subset of ~work_cap multiplies scaled by the row ratio."""
@@ -424,14 +448,15 @@ def cpu_d12(work_cap=1e9, groups=None):
     from paper_2011_02621_b200.network import _path_for, _resolve_cuts, _ShapeNet
     from paper_2011_02621_b200.tns import evolve, init_state, psi_batch
 
-    circ = syc_circuit(D12["depth"])
+    pc = plan_cfg or D12
+    circ = syc_circuit(pc["depth"])
     fused = fuse_single_qubit_gates(circ)
-    phi = evolve(init_state(fused.graph, "0" * 53), fused, range(0, D12["split"]), "forward")
-    psi = psi_batch(fused, ["0" * 53], D12["split"])
+    phi = evolve(init_state(fused.graph, "0" * 53), fused, range(0, pc["split"]), "forward")
+    psi = psi_batch(fused, ["0" * 53], pc["split"])
     edges = {e: phi.bond_dims[e] * psi.bond_dims[e] for e in fused.graph.edges}
     sn = _ShapeNet(range(53), edges)
-    plan = _resolve_cuts(sn, D12["cuts"], D12["cap"])
-    path, _ = _path_for(sn, plan, D12["cap"])
+    plan = _resolve_cuts(sn, pc["cuts"], pc["cap"])
+    path, _ = _path_for(sn, plan, pc["cap"])
     legs = {q: fused.graph.node_edges(q) for q in range(53)}
     lay = O.reference_step_layouts(legs, edges, path, plan.cut_edges)
     return lay, edges, plan.slice_count, O
@@ -761,7 +786,7 @@ def run_reference(args, base):
     the reference's np.tensordot steps of one slice on row subsets (every
     path step once per group rotation: the path's steps are split into
     ``NG`` groups of similar sampled work and step i runs group i mod NG).
-    value = amplitudes/s from the mean sampled time per full rotation x 1024
+    value = amplitudes/s from the mean sampled time per full rotation x S
     slices; ms_per_step is the wall time of the steps actually run."""
     t0 = time.perf_counter()
     lay, edges, S, O = cpu_d12()
@@ -808,7 +833,7 @@ def dry_run(args, rank, world):
     of partial amplitudes, max-over-ranks timing -- no contraction."""
     import torch
 
-    S, k = 1024, args.slices_per_step
+    S, k = D12["slices"], args.slices_per_step
     t0 = time.perf_counter()
     part = torch.zeros(2, dtype=torch.float64)
     for i in range(args.steps):
@@ -887,6 +912,9 @@ def main():
                                              f"({spent:.1f} s measured, {tot:.0f} s per slice); x{S} slices"}
         nested = {}
         if args.nested:
+            r1 = run_d12(args, rank, world, dev, plan_cfg=D12_CAP31, steps=5, warmup=3, e2e=False)
+            free(r1)
+            nested["amplitudes_53q_depth12_cap31"] = r1
             for depth, B in ((10, 8), (8, 64)):
                 r2 = run_twosided(args, rank, world, dev, depth, B, steps=5, warmup=3)
                 free(r2)
