@@ -779,6 +779,140 @@ def cpu_cfg0(budget_s=5.0):
 
 
 # ---------------------------------------------------------------------------
+# square-lattice configs: configs[2] (5x4) and configs[3] (7x7)
+# ---------------------------------------------------------------------------
+SQUARE = {
+    # 5x4, 14 cycles: the deepest configs[2]-family circuit whose two-sided network runs unsliced (2^31 elements)
+    "amplitudes_cfg2_d14": dict(rows=5, cols=4, depth=14, split=7, cap=6, cuts=None, B=4, k=0, dtype="complex64",
+                                steps=3, warmup=1, verify=True),
+    "amplitudes_cfg2_d14_c128": dict(rows=5, cols=4, depth=14, split=7, cap=6, cuts=None, B=1, k=0,
+                                     dtype="complex128", steps=2, warmup=1, verify=True),
+    # configs[2] as written (16 cycles): 2^36-element intermediates unsliced; cheapest cut set found
+    # (tools/cut_search.py) is (4,8),(11,15): 16384 slices of 2^29 elements, 2.27e17 multiplies per amplitude
+    "amplitudes_cfg2_d16": dict(rows=5, cols=4, depth=16, split=8, cap=6, cuts=[(4, 8), (11, 15)], B=1, k=16,
+                                dtype="complex64", steps=3, warmup=1, verify=False),
+    # 7x7, 10 cycles: unsliced two-sided network, 2^33-element intermediates (two 64 GiB accumulators)
+    "amplitudes_cfg3_d10": dict(rows=7, cols=7, depth=10, split=5, cap=9, cuts=None, B=1, k=0, dtype="complex64",
+                                steps=3, warmup=1, verify=False),
+    # configs[3] as written (12 cycles, M = treewidth bound + 1 = 9, 2^30-element cap): 2^20 slices
+    "amplitudes_cfg3_d12": dict(rows=7, cols=7, depth=12, split=6, cap=9,
+                                cuts=[(20, 27), (19, 26), (18, 25), (17, 24)], B=1, k=256, dtype="complex64",
+                                steps=3, warmup=1, verify=False),
+}
+FP64_TENSOR_TFLOPS = 40.0      # B200 datasheet FP64 (tensor) rate: no measured value in MEASURED_PEAKS.json
+
+
+def run_square(args, rank, world, dev, name):
+    """One entry of SQUARE: whole amplitudes of B bitstrings per step (unsliced
+    plans, k = 0) or k slices of one bitstring per step (sliced plans; value =
+    k * steps / S / t as in the headline).  ``verify``: amplitudes of the timed
+    bitstrings against the dense state vector (oracle, outside the timed region)."""
+    import torch
+
+    from paper_2011_02621_b200 import generate_lattice, pattern_rqc, square_patterns
+    from paper_2011_02621_b200.network import TwoSidedEngine
+
+    c = SQUARE[name]
+    hbm, bf16, bf16_sus, _ = peaks()
+    n = c["rows"] * c["cols"]
+    graph = generate_lattice("square", c["rows"], c["cols"])
+    circ = pattern_rqc(graph, square_patterns(c["rows"], c["cols"]), c["depth"], seed=SEED)
+    t0 = time.perf_counter()
+    eng = TwoSidedEngine(circ, split_cycle=c["split"], cuts=c["cuts"], max_rank=c["cap"], dtype=c["dtype"], device=dev,
+                         max_batch_elems=1 if c["k"] == 0 else None)
+    setup_s = time.perf_counter() - t0
+    B, k, steps, warmup = c["B"], c["k"], c["steps"], c["warmup"]
+    bits = random_bits(n, B * world, 300 + c["depth"])
+    mine = bits[rank * B:(rank + 1) * B]
+    ex = eng.prepare(mine)
+    plan = eng.plan
+    S = plan.slice_count
+    tdt = torch.complex64 if c["dtype"] == "complex64" else torch.complex128
+    amp = torch.zeros(B, dtype=tdt, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def one_step(i):
+        if k:
+            lo = ((i * world + rank) * k) % S
+            eng.run(ex, B, amp, slices=range(lo, min(lo + k, S)))
+        else:
+            eng.run(ex, B, amp)
+
+    for i in range(warmup):
+        one_step(i)
+    barrier(world)
+    torch.cuda.synchronize(dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    with ClockSampler(dev.index) as clk:
+        for i, (e0, e1) in enumerate(evs):
+            e0.record(stream)
+            one_step(warmup + i)
+            e1.record(stream)
+        torch.cuda.synchronize(dev)
+    t = allreduce_max(sum(a.elapsed_time(b) for a, b in evs) * 1e-3, world, dev)
+    value = world * B * steps / t if not k else world * k * steps / S / t
+    z = ex._steps[0].Z
+    times = step_times(ex, plan, dev)
+    itemsize = 8 if c["dtype"] == "complex64" else 16
+    if c["dtype"] == "complex64":
+        roof = path_roofline(plan, times, z, itemsize, hbm, bf16, bf16_sus)
+    else:
+        # complex128: GEMM steps on FP64 DMMA (mma.sync m8n8k4.f64, 4 real products per complex product)
+        tot = rf = gt = gf = 0.0
+        for sp, tt in zip(plan.steps, times):
+            by = (sp.M * sp.K + sp.M * sp.N) * itemsize * z
+            fl = 8.0 * sp.M * sp.K * sp.N * z
+            tot += tt
+            rf += max(by / (hbm * 1e9), fl / (FP64_TENSOR_TFLOPS * 1e12))
+            if is_gemm_step(sp, z):
+                gt += tt
+                gf += fl
+        roof = {"bound": "tensor", "achieved": gf / gt / 1e12 if gt else 0.0, "peak": FP64_TENSOR_TFLOPS,
+                "unit": "TFLOP/s", "frac": gf / gt / 1e12 / FP64_TENSOR_TFLOPS if gt else None,
+                "kernel": "tnc::k_dmma_c128 (mma.sync.m8n8k4.f64 DMMA, complex as 4 real products)",
+                "peak_source": "B200 datasheet FP64 tensor rate (no measured FP64 value in MEASURED_PEAKS.json)",
+                "kernel_share_of_step": gt / tot if tot else None, "path_roofline_frac": rf / tot if tot else None,
+                "traffic": None}
+    cuts_txt = ",".join(f"({a},{b})" for a, b in c["cuts"]) if c["cuts"] else "none"
+    res = {"value": value, "unit": "amplitudes/s", "ms_per_step": 1e3 * t / steps, "steps": steps, "warmup": warmup,
+           "scaling": "weak", "roofline": roof, "clocks": clk.summary(), "dtype": c["dtype"],
+           "gpu_launches": launches_per_pass(plan, z) * len(ex.chunks(B, range(S) if not k else range(k))) * steps,
+           "config": {"workload": f"{c['rows']}x{c['cols']} square lattice, {c['depth']} cycles (gate set and pattern "
+                                  f"rule of configs[0]), two-sided split {c['split']}, rank cap {c['cap']}, cut edges "
+                                  f"{cuts_txt}; one step = " +
+                                  (f"{B} whole amplitude(s) per rank" if not k else f"{k} of {S} slices of one bitstring"),
+                      "dtype": c["dtype"], "slices_per_amplitude": S, "multiplies_per_amplitude": plan.multiplies,
+                      "max_elems": plan.max_elems, "path_steps": len(plan.steps), "host_setup_s": setup_s}}
+    if k:
+        res["s_per_amplitude_per_gpu"] = t / steps * S / k
+    if c["verify"] and rank == 0:
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import tn_oracle as O  # checker only, outside the timed region
+
+        ref = O.statevector_amplitudes(circ, "0" * n, mine)
+        got = amp.cpu().numpy().astype(np.complex128)
+        res["rel_l2_vs_statevector"] = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
+    if args.e2e and not k:
+        eng.amplitudes(mine)
+        torch.cuda.synchronize(dev)
+        barrier(world)
+        es = max(1, min(steps, 2))
+        eng._bra_cache = None
+        t0 = time.perf_counter()
+        for _ in range(es):
+            eng._bra_cache = None                      # every step: host bra evolution, H2D, contraction, D2H
+            eng.amplitudes(mine)
+        te = allreduce_max(time.perf_counter() - t0, world, dev)
+        res["e2e"] = {"value": world * B * es / te, "unit": "amplitudes/s", "steps": es,
+                      "h2d_bytes_per_step": B * (eng._overlap.h2d_bytes_per_bitstring + n),
+                      "d2h_bytes_per_step": B * 16,
+                      "path": "TwoSidedEngine.amplitudes(bitstrings) -> host amplitudes (host bra evolution, pinned "
+                              "H2D of the bra sites, overlap sites and contraction on the GPU, D2H)"}
+    res["_engine"] = eng
+    return res
+
+
+# ---------------------------------------------------------------------------
 # reference arm (CPU oracle port, same config as the headline)
 # ---------------------------------------------------------------------------
 def run_reference(args, base):
@@ -856,7 +990,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="d12", choices=["d12", "d10", "d8", "sweep", "cfg0"])
+    ap.add_argument("--workload", default="d12", choices=["d12", "d10", "d8", "sweep", "cfg0", "square"])
     ap.add_argument("--slices-per-step", type=int, default=1)
     ap.add_argument("--limit", type=int, default=SWEEP_LIMIT)
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
@@ -921,6 +1055,10 @@ def main():
                 if cpu_here and depth == 8:         # a depth-10 amplitude takes minutes on the host
                     r2["cpu_baseline"] = cpu_twosided(8, 2, 20.0)
                 nested[f"amplitudes_53q_depth{depth}_twosided"] = r2
+            for name in SQUARE:
+                r5 = run_square(args, rank, world, dev, name)
+                free(r5)
+                nested[name] = r5
             r3 = run_sweep(args, rank, world, dev, steps=3, warmup=2)
             if cpu_here:
                 r3["cpu_baseline"] = cpu_sweep(args, r3["detail"], 10.0)
@@ -938,6 +1076,14 @@ def main():
         free(res)
         if cpu_here and depth == 8:
             res["cpu_baseline"] = cpu_twosided(8, 2, 20.0)
+    elif args.workload == "square":
+        res = {}
+        for name in SQUARE:
+            r5 = run_square(args, rank, world, dev, name)
+            free(r5)
+            res[name] = r5
+        first = res["amplitudes_cfg2_d14"]
+        res = dict({k: first[k] for k in ("value", "unit", "ms_per_step", "dtype", "config", "roofline", "clocks")}, **res)
     elif args.workload == "sweep":
         res = run_sweep(args, rank, world, dev, args.steps, args.warmup)
         if cpu_here:

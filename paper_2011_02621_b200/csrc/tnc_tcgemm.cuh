@@ -68,6 +68,7 @@ struct GemmDesc {
   int64_t f_dim[TNC_MAX_LEGS], f_cstride[TNC_MAX_LEGS];
   const int64_t* c_noff;         // [N]
   unsigned int* progress;        // pair kernel: items whose A loads have been issued, summed over CTAs (zeroed by the host)
+  float comp, _pad7;             // 1 + TG_RZ_LOSS * (MMA accumulations per accumulator element), applied by the epilogue
 };
 
 // warps: converters [0, CONVW), epilogue [CONVW, MMA), MMA issuer, A and B producers;
@@ -142,6 +143,16 @@ __device__ __forceinline__ void mbar_wait_idle(uint64_t* bar, uint32_t phase) {
       "bra WAIT_%=;\n\t"
       "DONE_%=:\n\t}" ::"r"(smem_u32(bar)), "r"(phase), "r"(4000u) : "memory");
 }
+
+// tcgen05.mma adds each instruction's dot product to the fp32 accumulator with
+// truncation (round toward zero), so every accumulation loses on average
+// 1.6e-8 of the accumulator's magnitude (measured, tools/rz_bias_probe.py: the
+// result of a step shrinks by 3.03e-9 K with 3 accumulations per 16 k (3M
+// fp16), 6.04e-9 K with 6 (4M fp16), 1.21e-8 K with 6 per 8 k (3xTF32), for
+// every tile shape).  Over the ~25 GEMM steps of a path the shrink adds up to
+// 1e-4 of the amplitude, the whole complex64 tolerance; the epilogue scales
+// the result by 1 + TG_RZ_LOSS * accumulations, which removes the mean loss.
+constexpr float TG_RZ_LOSS = 1.616e-8f;
 
 // per combo (blockIdx.x): max |re|, |im| over the site block (F16 scale of
 // B'); blockIdx.y strides over K rows, atomicMax into the zeroed bscale
@@ -475,7 +486,7 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
     // innermost result leg is a free leg: consecutive rows are contiguous)
     const bool staged = (p.c_rows_contig || p.n_contig || (p.N > 1 && p.c_noff[1] == p.c_noff[0] + 1));
     const int cfirst = alt ? 0 : eg * 16, cstep = alt ? 16 : 16 * EPIG;
-    float inv = 1.f, inv2 = 1.f;
+    float inv = p.comp, inv2 = 1.f;
     int64_t inv_z = -1;
     const uint32_t stg_s = smem_u32(stg);
     for (int it = alt ? eg : 0; it < nitems; it += alt ? EPIG : 1) {
@@ -513,7 +524,7 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
           inv_z = z;
           // two exact power-of-two factors: their product can leave the fp32 range
           // when both tensors are tiny although every result is representable
-          inv = 1.f / op_scale(__ldg(p.amax_in + z), G3);
+          inv = p.comp / op_scale(__ldg(p.amax_in + z), G3);
           inv2 = 1.f / op_scale(__ldg(p.bscale + gemm_combo(p, z)), G3);
         }
       }
@@ -838,6 +849,8 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
       ares = f16 && p.tiles_n > 1 && TS * 2 * p.NT + p.nchunk * acols <= 512 && p.nchunk <= TC_MAX_STAGES;
     }
     p.g3 = (f16 && p.NT == 128 && !ares) ? 1 : 0;
+    // accumulations into each accumulator element over the K loop (see TG_RZ_LOSS)
+    p.comp = 1.f + TG_RZ_LOSS * (float)(f16 ? (d.K / 16) * (p.g3 ? 3 : 6) : (d.K / 8) * 6);
     // stages: fill the shared-memory budget
     int RS = 4, BS = 3;
     const size_t budget = 226 * 1024;

@@ -344,7 +344,7 @@ k_tc_gemm2(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorM
       const int64_t n0 = nt * NT + eg * 64;        // first column of this warp
       if (z != inv_z) {
         inv_z = z;
-        inv = 1.f / op_scale(__ldg(p.amax_in + z), 1);
+        inv = p.comp / op_scale(__ldg(p.amax_in + z), 1);
         inv2 = 1.f / op_scale(__ldg(p.bscale + gemm_combo(p, z)), 1);
       }
       float vmax = 0.f;

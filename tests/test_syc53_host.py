@@ -112,3 +112,26 @@ def test_psi_batch_rank_mismatch_detected():
     st = TNSBatch(g, {0: t0, 1: t1}, {e: 2})
     with pytest.raises(RankMismatch):
         _compress_batch(st, e, 1e-12)
+
+
+SQUARE = json.loads((GOLDEN / "square.json").read_text())["cases"]
+
+
+@pytest.mark.parametrize("name", [c["name"] for c in SQUARE])
+def test_cfg3_7x7_plan_bit_exact(name):
+    """configs[3] family (7x7, reference default rank cap = treewidth bound + 1):
+    path, score, cut plan, peak rank and multiplies equal the reference's."""
+    case = next(c for c in SQUARE if c["name"] == name)
+    r = case["results"][0]
+    c, phi, psi, edges = _network(case, r["out"])
+    n = c.num_qubits
+    sn = _ShapeNet(range(n), edges)
+    cuts = [tuple(e) for e in case["cuts"]] if case["cuts"] else None
+    plan = _resolve_cuts(sn, cuts, case["max_rank"])
+    path, score = _path_for(sn, plan, case["max_rank"])
+    assert path == r["path"] and str(score) == r["path_score"]
+    cp = ContractionPlan(NetworkSpec(list(range(n)), edges, {q: c.graph.node_edges(q) for q in range(n)}),
+                         path, plan.cut_edges)
+    assert cp.peak_rank == r["peak_rank"]
+    assert str(cp.multiplies) == r["multiplies"]
+    assert cp.slice_count == r["slice_count"]
