@@ -54,6 +54,8 @@ sys.path.insert(0, str(ROOT))
 METRIC = "amplitudes/sec (53q, depth 12) at 1/2/4/8 GPUs; contraction % of roofline"
 D12 = {"depth": 12, "split": 6, "cap": 12, "cuts": [(9, 14), (2, 8)], "slices": 256, "elem_log2": 33}
 D12_CAP31 = {"depth": 12, "split": 6, "cap": 12, "cuts": [(45, 49), (38, 45)], "slices": 1024, "elem_log2": 31}
+# 11 cycles (reference default split 5): one cut edge, 16 slices, 4.45e14 multiplies per amplitude
+D11 = {"depth": 11, "split": 5, "cap": 12, "cuts": [(45, 49)], "slices": 16, "elem_log2": 33}
 SWEEP_LIMIT = 1 << 32          # elements per operand (complex64: 32 GiB)
 SEED = 0
 NCU_D12_PROFILE = "profiles/r02f_ncu_d12_pair.json"   # ncu --set full of the top GEMM step (dram bytes)
@@ -318,9 +320,10 @@ def d12_engine(dev, max_batch_elems=1, plan_cfg=None):
 def d12_config(eng=None, k=1, plan_cfg=None):
     pc = plan_cfg or D12
     cuts = ",".join(f"({a},{b})" for a, b in pc["cuts"])
-    cfg = {"workload": "configs[4]: 53-qubit Sycamore (ABCDCDAB, fSim(pi/2, pi/6)), 12 cycles, two-sided split 6, "
-                       f"rank cap 12, sliced over {cuts}; one step = 1 bitstring x {k} slice(s) per rank",
-           "dtype": "complex64", "depth": 12, "split_cycle": 6, "max_rank": 12,
+    cfg = {"workload": f"configs[4]: 53-qubit Sycamore (ABCDCDAB, fSim(pi/2, pi/6)), {pc['depth']} cycles, two-sided "
+                       f"split {pc['split']}, rank cap 12, sliced over {cuts}; one step = 1 bitstring x {k} slice(s) "
+                       "per rank",
+           "dtype": "complex64", "depth": pc["depth"], "split_cycle": pc["split"], "max_rank": 12,
            "cut_edges": [list(e) for e in pc["cuts"]], "slices_per_amplitude": pc["slices"],
            "largest_intermediate_log2_elems": pc["elem_log2"],
            "cap_note": "configs[4] names a 2^30-element cap; the cheapest cut set found for it (tools/cut_search.py: "
@@ -328,6 +331,8 @@ def d12_config(eng=None, k=1, plan_cfg=None):
                        "1.5e16 (2^33) / 2.0e16 (2^31): the cap is sized for the B200's 180 GB instead",
            "slices_per_step_per_rank": k, "circuit_seed": SEED,
            "l2": f"inputs larger than L2 (2 x 2^{pc['elem_log2']}-element complex64 ping-pong accumulators)"}
+    if pc["depth"] != 12:
+        cfg.pop("cap_note")
     return cfg
 
 
@@ -1049,6 +1054,9 @@ def main():
             r1 = run_d12(args, rank, world, dev, plan_cfg=D12_CAP31, steps=5, warmup=3, e2e=False)
             free(r1)
             nested["amplitudes_53q_depth12_cap31"] = r1
+            r1 = run_d12(args, rank, world, dev, plan_cfg=D11, steps=5, warmup=3, e2e=False)
+            free(r1)
+            nested["amplitudes_53q_depth11"] = r1
             for depth, B in ((10, 8), (8, 64)):
                 r2 = run_twosided(args, rank, world, dev, depth, B, steps=5, warmup=3)
                 free(r2)

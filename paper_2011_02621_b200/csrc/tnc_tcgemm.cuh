@@ -955,8 +955,26 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
         attr2 |= 1ull << (adev2 & 63);
       }
       const int64_t W = p.Z * ((p.tiles_m + 1) / 2) * p.tiles_n;
-      const int64_t npairs = std::min<int64_t>(sms / 2, W);
       const size_t smem2 = tg2_smem_bytes(p.RS, p.BS, p.cn_smem ? d.N : 0);
+      // every CTA of the grid must be resident (the drift bound spins on the
+      // other CTAs' progress): at most the clusters the device can hold at once
+      int max_pairs = sms / 2;
+      {
+        cudaLaunchConfig_t lc;
+        memset(&lc, 0, sizeof lc);
+        lc.gridDim = dim3((unsigned)sms & ~1u);
+        lc.blockDim = dim3(TG2_THREADS);
+        lc.dynamicSmemBytes = smem2;
+        cudaLaunchAttribute la;
+        la.id = cudaLaunchAttributeClusterDimension;
+        la.val.clusterDim.x = 2; la.val.clusterDim.y = 1; la.val.clusterDim.z = 1;
+        lc.attrs = &la;
+        lc.numAttrs = 1;
+        int nc = 0;
+        if (cudaOccupancyMaxActiveClusters(&nc, k_tc_gemm2, &lc) == cudaSuccess && nc > 0) max_pairs = std::min(max_pairs, nc);
+        else cudaGetLastError();
+      }
+      const int64_t npairs = std::min<int64_t>(max_pairs, W);
       k_tc_gemm2<<<(unsigned)(2 * npairs), TG2_THREADS, smem2, s>>>(p, tm, tmb);
     } else if (p.g3) k_tc_gemm<16, true, true><<<(unsigned)grid, TG_THREADS_G3, smem, s>>>(p, tm);
     else if (f16) k_tc_gemm<16, true><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm);

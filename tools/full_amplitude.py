@@ -42,6 +42,9 @@ def main():
     ap.add_argument("--dtype", default="complex64")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--json", default=None)
+    ap.add_argument("--slice-lo", type=int, default=0, help="first slice of this run (a run cut off by a time "
+                    "limit is continued from its JSON's slices_done; the partial sums add)")
+    ap.add_argument("--slice-hi", type=int, default=-1)
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
     n = args.rows * args.cols
@@ -63,8 +66,10 @@ def main():
         doc["statevector"] = [[float(a.real), float(a.imag)] for a in ref]
     tdt = torch.complex64 if args.dtype == "complex64" else torch.complex128
     amp = torch.zeros(args.nbits, dtype=tdt, device=dev)
-    for lo in range(0, S, args.chunk):
-        hi = min(S, lo + args.chunk)
+    s_hi = S if args.slice_hi < 0 else min(S, args.slice_hi)
+    doc["slice_range"] = [args.slice_lo, s_hi]
+    for lo in range(args.slice_lo, s_hi, args.chunk):
+        hi = min(s_hi, lo + args.chunk)
         torch.cuda.synchronize()
         t1 = time.perf_counter()
         eng.run(ex, args.nbits, amp, slices=range(lo, hi), accumulate=True)
@@ -73,15 +78,15 @@ def main():
         doc["slices_done"] = hi
         a = amp.cpu().numpy().astype(np.complex128)
         doc["partial_sum"] = [[float(x.real), float(x.imag)] for x in a]
-        doc["est_total_s"] = doc["gpu_s"] * S / hi
+        doc["est_total_s"] = doc["gpu_s"] * S / (hi - args.slice_lo)
         if args.json:
             with open(args.json, "w") as f:
                 json.dump(doc, f, indent=1)
         print(f"slices {hi}/{S}  {doc['gpu_s']:.1f} s  est total {doc['est_total_s']:.0f} s", flush=True)
     got = amp.cpu().numpy().astype(np.complex128)
     doc["amplitude"] = [[float(x.real), float(x.imag)] for x in got]
-    doc["amplitudes_per_s"] = args.nbits / doc["gpu_s"]
-    if ref is not None:
+    doc["amplitudes_per_s"] = args.nbits / doc["gpu_s"] * (s_hi - args.slice_lo) / S
+    if ref is not None and args.slice_lo == 0 and s_hi == S:
         doc["rel_l2_vs_statevector"] = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
         print("rel L2 vs state vector:", doc["rel_l2_vs_statevector"])
     if args.json:
