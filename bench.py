@@ -794,14 +794,14 @@ SQUARE = {
                                      dtype="complex128", steps=2, warmup=1, verify=True),
     # configs[2] as written (16 cycles): 2^36-element intermediates unsliced; cheapest cut set found
     # (tools/cut_search.py) is (4,8),(11,15): 16384 slices of 2^29 elements, 2.27e17 multiplies per amplitude
-    "amplitudes_cfg2_d16": dict(rows=5, cols=4, depth=16, split=8, cap=6, cuts=[(4, 8), (11, 15)], B=1, k=16,
+    "amplitudes_cfg2_d16": dict(rows=5, cols=4, depth=16, split=8, cap=6, cuts=[(4, 8), (11, 15)], B=1, k=8,
                                 dtype="complex64", steps=3, warmup=1, verify=False),
     # 7x7, 10 cycles: unsliced two-sided network, 2^33-element intermediates (two 64 GiB accumulators)
     "amplitudes_cfg3_d10": dict(rows=7, cols=7, depth=10, split=5, cap=9, cuts=None, B=1, k=0, dtype="complex64",
                                 steps=3, warmup=1, verify=False),
     # configs[3] as written (12 cycles, M = treewidth bound + 1 = 9, 2^30-element cap): 2^20 slices
     "amplitudes_cfg3_d12": dict(rows=7, cols=7, depth=12, split=6, cap=9,
-                                cuts=[(20, 27), (19, 26), (18, 25), (17, 24)], B=1, k=256, dtype="complex64",
+                                cuts=[(20, 27), (19, 26), (18, 25), (17, 24)], B=1, k=64, dtype="complex64",
                                 steps=3, warmup=1, verify=False),
 }
 FP64_TENSOR_TFLOPS = 40.0      # B200 datasheet FP64 (tensor) rate: no measured value in MEASURED_PEAKS.json

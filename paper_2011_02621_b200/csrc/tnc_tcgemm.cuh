@@ -72,11 +72,11 @@ struct GemmDesc {
 };
 
 // warps: converters [0, CONVW), epilogue [CONVW, MMA), MMA issuer, A and B producers;
-// 3M tiles: 8 converter + 8 epilogue warps (19), otherwise 15 warps in all
+// fp16-split tiles: 8 converter + 8 epilogue warps (19), 3xTF32: 8 + 4 (15 warps in all)
 constexpr int TG_THREADS = 15 * 32;
 constexpr int TG_THREADS_G3 = 19 * 32;
 constexpr int TG_EPI_WARP0 = 8;
-__host__ __device__ constexpr int tg_mma_warp(bool g3) { return g3 ? 16 : 12; }
+__host__ __device__ constexpr int tg_mma_warp(bool f16) { return f16 ? 16 : 12; }
 constexpr int TG_MAX_RS = 8, TG_MAX_BS = 8;
 constexpr int TG_EPI_PITCH = 16 * 8 + 16;      // staged row: 16 complex + 16 B pad
 
@@ -266,7 +266,7 @@ __device__ __forceinline__ uint32_t f16_idesc(int n_real) {
 // columns, re = T1 - T2, im = T3 - T1 - T2 in the epilogue: 9 instead of 12
 // N = NT MMA units per chunk (wide tiles, NT = 128, one accumulator stage)
 template <int KC, bool F16, bool G3 = false>
-__global__ void __launch_bounds__(G3 ? TG_THREADS_G3 : TG_THREADS, 1)
+__global__ void __launch_bounds__(F16 ? TG_THREADS_G3 : TG_THREADS, 1)
 k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMap tmA) {
   static_assert(!F16 || KC == 16, "F16 mode needs 16-complex chunks (K = 16 per MMA)");
   static_assert(!G3 || F16, "3M products run on the fp16-split operands");
@@ -284,11 +284,11 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
   // 2*KC (fp16: two values per column) columns
   constexpr uint32_t ACOLS = G3 ? 3 * KC : (F16 ? 2 * KC : 4 * KC);
   constexpr int NACC = G3 ? 3 : 2;                 // accumulator blocks of NT columns per stage
-  // warp roles: converters [0, CONVW), epilogue [CONVW, 12) in EPIG groups of
-  // four (one per TMEM lane quadrant; groups split the columns), 12 MMA, 13/14
-  // producers.  fp16 conversion is cheap, so F16 gives the epilogue 8 warps.
-  constexpr int TG_MMA_WARP = tg_mma_warp(G3), TG_APROD_WARP = TG_MMA_WARP + 1, TG_BPROD_WARP = TG_MMA_WARP + 2;
-  constexpr int CONVW = (F16 && !G3) ? 4 : 8;
+  // warp roles: converters [0, 8), epilogue [8, MMA) in EPIG groups of four
+  // (one per TMEM lane quadrant; groups split the columns), then the MMA
+  // issuer and the two producers.
+  constexpr int TG_MMA_WARP = tg_mma_warp(F16), TG_APROD_WARP = TG_MMA_WARP + 1, TG_BPROD_WARP = TG_MMA_WARP + 2;
+  constexpr int CONVW = 8;
   constexpr int EPIW = TG_MMA_WARP - CONVW;
   constexpr int EPIG = EPIW / 4;
   // narrow tiles (NT <= 32, short epilogue per item, latency-bound): the
@@ -364,8 +364,8 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
 
   if (warp < CONVW) {
     // ---------------- converters: raw smem -> tf32/fp16 hi/lo -> TMEM ----------------
-    // warp w converts rows 32*(w%4).. (its TMEM lane quadrant); tf32: complex
-    // [h*KC/2, (h+1)*KC/2) with h = w/4 (8 warps), F16: all KC complex (4 warps).
+    // warp w converts rows 32*(w%4).. (its TMEM lane quadrant), complex
+    // [h*KC/2, (h+1)*KC/2) with h = w/4.
     const int h = warp >> 2;
     const int r = (warp & 3) * 32 + lane;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
@@ -410,25 +410,26 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
           tmem_st<4>(tmem + lane_base + col + 32, il);
           tmem_st<4>(tmem + lane_base + col + 40, sl);
         } else if constexpr (F16) {
-          // 16 complex -> 16 Ar and 16 Ai values, hi/lo fp16, two per TMEM column
-          uint32_t rh[KC / 2], ih[KC / 2], rl[KC / 2], il[KC / 2];
+          // warp (quadrant, half h): complex [8h, 8h + 8) of its 32 rows -> Ar, Ai
+          // hi/lo fp16, two per TMEM column (4 per plane)
+          uint32_t rh[4], ih[4], rl[4], il[4];
 #pragma unroll
-          for (int q = 0; q < KC / 2; ++q) {
-            const uint32_t off = (uint32_t)(r * RB + 16 * q);
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t off = (uint32_t)(r * RB + 16 * (4 * h + q));
             const uint32_t phys = off ^ (((off >> 7) & SWM) << 4);
             float4 x;
             asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(x.x), "=f"(x.y), "=f"(x.z), "=f"(x.w) : "r"(src + phys));
-            split_f16x2(x.x * sA, x.z * sA, rh[q], rl[q]);   // re of complex 2q, 2q+1
-            split_f16x2(x.y * sA, x.w * sA, ih[q], il[q]);   // im
+            split_f16x2_cvt(x.x * sA, x.z * sA, rh[q], rl[q]);   // re of complex 2q, 2q+1
+            split_f16x2_cvt(x.y * sA, x.w * sA, ih[q], il[q]);   // im
           }
           mbar_wait_spin(&aempty[astage], aph ^ 1);
           tc_fence_after();
           // stage layout: [Ar_hi 8 | Ai_hi 8 | Ar_lo 8 | Ai_lo 8] columns (16 k each)
-          const uint32_t col = A0 + (uint32_t)astage * ACOLS;
-          tmem_st<KC / 2>(tmem + lane_base + col, rh);
-          tmem_st<KC / 2>(tmem + lane_base + col + 8, ih);
-          tmem_st<KC / 2>(tmem + lane_base + col + 16, rl);
-          tmem_st<KC / 2>(tmem + lane_base + col + 24, il);
+          const uint32_t col = A0 + (uint32_t)astage * ACOLS + 4 * h;
+          tmem_st<4>(tmem + lane_base + col, rh);
+          tmem_st<4>(tmem + lane_base + col + 8, ih);
+          tmem_st<4>(tmem + lane_base + col + 16, rl);
+          tmem_st<4>(tmem + lane_base + col + 24, il);
         }
         if constexpr (F16) {
           tmem_wait_st();
@@ -977,7 +978,7 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
       const int64_t npairs = std::min<int64_t>(max_pairs, W);
       k_tc_gemm2<<<(unsigned)(2 * npairs), TG2_THREADS, smem2, s>>>(p, tm, tmb);
     } else if (p.g3) k_tc_gemm<16, true, true><<<(unsigned)grid, TG_THREADS_G3, smem, s>>>(p, tm);
-    else if (f16) k_tc_gemm<16, true><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm);
+    else if (f16) k_tc_gemm<16, true><<<(unsigned)grid, TG_THREADS_G3, smem, s>>>(p, tm);
     else if (KC == 16) k_tc_gemm<16, false><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm);
     else k_tc_gemm<8, false><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm);
     const bool ok = cudaGetLastError() == cudaSuccess;
