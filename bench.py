@@ -23,8 +23,12 @@ S / t (whole-job amplitudes/s; per-rank work fixed: "weak").  Every slice
 has the same shapes and path, so a step is an exact 1/S-of-an-amplitude
 unit of work; ``tools/net_probe.py --full`` runs whole amplitudes.
 
-Nested entries (same JSON line): two-sided 53q depth 10 and depth 8 (whole
-amplitudes, bitstring batches), the configs[1] pairwise sweep, configs[0].
+Nested entries (same JSON line, single-GPU runs only): the 2^31 plan and 53q
+depth 11 (slices), two-sided 53q depth 10 and depth 8 (whole amplitudes,
+bitstring batches), configs[2] (5x4: depth 14 whole amplitudes in complex64 and
+complex128 checked against the state vector, depth 16 slices), configs[3] (7x7:
+depth 10 whole amplitudes, depth 12 slices), the configs[1] pairwise sweep,
+configs[0].
 
 Timing: W untimed warm-up steps, then K steps, each bracketed by CUDA events
 on the launching stream; barrier + synchronize around the timed region; max
@@ -1050,7 +1054,7 @@ def main():
                                              "operand layout over a row subset of <= 1e9 multiplies, scaled by rows "
                                              f"({spent:.1f} s measured, {tot:.0f} s per slice); x{S} slices"}
         nested = {}
-        if args.nested:
+        if args.nested and world == 1:          # N > 1 runs time the headline only (the driver's scaling sweep)
             r1 = run_d12(args, rank, world, dev, plan_cfg=D12_CAP31, steps=5, warmup=3, e2e=False)
             free(r1)
             nested["amplitudes_53q_depth12_cap31"] = r1
