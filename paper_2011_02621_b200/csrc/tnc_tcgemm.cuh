@@ -68,7 +68,8 @@ struct GemmDesc {
   int64_t f_dim[TNC_MAX_LEGS], f_cstride[TNC_MAX_LEGS];
   const int64_t* c_noff;         // [N]
   unsigned int* progress;        // pair kernel: items whose A loads have been issued, summed over CTAs (zeroed by the host)
-  float comp, _pad7;             // 1 + TG_RZ_LOSS * (MMA accumulations per accumulator element), applied by the epilogue
+  float comp;                    // 1 + TG_RZ_LOSS * (MMA accumulations per accumulator element), applied by the epilogue
+  int32_t kseg;                  // pair kernel: chunks per K segment (TG2_KSEG)
 };
 
 // warps: converters [0, CONVW), epilogue [CONVW, MMA), MMA issuer, A and B producers;
@@ -893,6 +894,7 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
       while (RS + 1 <= TG2_MAX_RS && tg2_smem_bytes(RS + 1, BS, cn2) <= budget) ++RS;
       if (tg2_smem_bytes(RS, BS, cn2) > budget) return 0;
       p.RS = RS; p.BS = BS;
+      p.kseg = TG2_KSEG;
     }
     unsigned char* bp = nullptr;
     pool_keep();

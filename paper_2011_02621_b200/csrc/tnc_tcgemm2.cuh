@@ -33,6 +33,9 @@ constexpr uint32_t TG2_BSTAGE = 6 * TG2_BBLK;          // [Br | Bi | Bs] hi, lo 
 constexpr uint32_t TG2_EBUF = 32 * 128;                // one warp round: 32 rows x 16 complex
 constexpr uint32_t TG2_ESTAGE = 8 * 3 * TG2_EBUF;      // 8 warps x 3 rounds: 96 KB
 constexpr int TG2_MAX_RS = 8, TG2_MAX_BS = 8;
+// chunks (16 complex of K each) per K segment: 2048 complex -- the truncation error of one segment's
+// accumulation chain is 3.7e-6 of the result (1.2e-4 at K = 65536 unsegmented, tools/rz_bias_probe.py)
+constexpr int TG2_KSEG = 128;
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
   uint32_t r;
@@ -133,14 +136,31 @@ __device__ __forceinline__ uint32_t tg2_piece(uint32_t buf_s, int row, int piece
 
 // result stores: streaming (evict-first) so that the result does not push the
 // A rows that other column tiles are about to re-read out of L2
-__device__ __forceinline__ void tg2_st4(float4* dst, float4 v) { __stcs(dst, v); }
-__device__ __forceinline__ void tg2_st2(float2* dst, float2 v) { __stcs(dst, v); }
+// `acc`: a later K segment of the tile -- the partial product is added to the
+// stored one in fp32 round-to-nearest (the same thread stored it);
+// `vmax`: max |re|, |im| of the final values (tracked on the last segment)
+__device__ __forceinline__ void tg2_st4(float4* dst, float4 v, bool acc, float& vmax) {
+  if (acc) {
+    const float4 o = *dst;
+    v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+    vmax = fmaxf(vmax, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+  }
+  __stcs(dst, v);
+}
+__device__ __forceinline__ void tg2_st2(float2* dst, float2 v, bool acc, float& vmax) {
+  if (acc) {
+    const float2 o = *dst;
+    v.x += o.x; v.y += o.y;
+    vmax = fmaxf(vmax, fmaxf(fabsf(v.x), fabsf(v.y)));
+  }
+  __stcs(dst, v);
+}
 
 // the warp's 32 rows x 16 columns [n0c0, n0c0 + ncols) of the result, from a
 // staged round buffer to global memory (layouts as k_tc_gemm's epilogue)
 __device__ __forceinline__ void tg2_flush(const GemmDesc& p, uint32_t buf_s, int lane, int q, int64_t mt, int64_t row,
                                           int64_t oc, float2* O, int64_t n0c0, int ncols, const int32_t* cn_s,
-                                          bool staged) {
+                                          bool staged, bool acc, float& vmax) {
   if (staged) {
     if (p.blk_contig && ncols == 16 && mt * 128 + q * 32 + 32 <= p.M) {
       const int64_t oc0 = __shfl_sync(0xffffffffu, oc, 0);
@@ -151,7 +171,7 @@ __device__ __forceinline__ void tg2_flush(const GemmDesc& p, uint32_t buf_s, int
         float4 v;
         asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                      : "r"(tg2_piece(buf_s, c >> 3, c & 7)) : "memory");
-        tg2_st4(dst + c, v);
+        tg2_st4(dst + c, v, acc, vmax);
       }
       return;
     }
@@ -172,10 +192,10 @@ __device__ __forceinline__ void tg2_flush(const GemmDesc& p, uint32_t buf_s, int
                      : "r"(tg2_piece(buf_s, lr, sub)) : "memory");
         float2* dst = O + ocr + a0;
         if (2 * sub + 1 < ncols && a1 == a0 + 1 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-          tg2_st4(reinterpret_cast<float4*>(dst), v);
+          tg2_st4(reinterpret_cast<float4*>(dst), v, acc, vmax);
         } else {
-          tg2_st2(dst, make_float2(v.x, v.y));
-          if (2 * sub + 1 < ncols) tg2_st2(O + ocr + a1, make_float2(v.z, v.w));
+          tg2_st2(dst, make_float2(v.x, v.y), acc, vmax);
+          if (2 * sub + 1 < ncols) tg2_st2(O + ocr + a1, make_float2(v.z, v.w), acc, vmax);
         }
       }
     }
@@ -190,11 +210,11 @@ __device__ __forceinline__ void tg2_flush(const GemmDesc& p, uint32_t buf_s, int
                    : "r"(tg2_piece(buf_s, lane, u)) : "memory");
       if (2 * u < ncols) {
         const int64_t n = n0c0 + 2 * u;
-        tg2_st2(O + oc + (p.cn_smem ? (int64_t)cn_s[n] : p.c_noff[n]), make_float2(v.x, v.y));
+        tg2_st2(O + oc + (p.cn_smem ? (int64_t)cn_s[n] : p.c_noff[n]), make_float2(v.x, v.y), acc, vmax);
       }
       if (2 * u + 1 < ncols) {
         const int64_t n = n0c0 + 2 * u + 1;
-        tg2_st2(O + oc + (p.cn_smem ? (int64_t)cn_s[n] : p.c_noff[n]), make_float2(v.z, v.w));
+        tg2_st2(O + oc + (p.cn_smem ? (int64_t)cn_s[n] : p.c_noff[n]), make_float2(v.z, v.w), acc, vmax);
       }
     }
   }
@@ -326,7 +346,8 @@ k_tc_gemm2(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorM
     float inv = 1.f, inv2 = 1.f;
     int64_t inv_z = -1;
     uint32_t tph = 0;
-    for (int it = 0; it < nitems; ++it, tph ^= 1) {
+    const int kseg = p.kseg;                     // chunks accumulated in TMEM before the sum leaves the tensor core
+    for (int it = 0; it < nitems; ++it) {
       int64_t z, mt, nt;
       item(it, z, mt, nt);
       const int64_t row = mt * 128 + r;
@@ -344,9 +365,17 @@ k_tc_gemm2(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorM
       const int64_t n0 = nt * NT + eg * 64;        // first column of this warp
       if (z != inv_z) {
         inv_z = z;
-        inv = p.comp / op_scale(__ldg(p.amax_in + z), 1);
+        inv = 1.f / op_scale(__ldg(p.amax_in + z), 1);
         inv2 = 1.f / op_scale(__ldg(p.bscale + gemm_combo(p, z)), 1);
       }
+      // K segments of at most kseg chunks: each is drained, scaled (with the
+      // truncation compensation of its own accumulation count) and added to
+      // the stored partial result in fp32 round-to-nearest, so the
+      // round-toward-zero chain inside the tensor core stays short
+      for (int c0 = 0; c0 < nchunk; c0 += kseg, tph ^= 1) {
+      const int c1 = min(nchunk, c0 + kseg);
+      const bool acc = c0 > 0, last = c1 == nchunk;
+      const float sc = inv * (1.f + TG_RZ_LOSS * (float)(3 * (c1 - c0)));
       float vmax = 0.f;
       mbar_wait_idle(tfull, tph);
       tc_fence_after();
@@ -367,8 +396,8 @@ k_tc_gemm2(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorM
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj) {          // re = T1 - T2, im = T3 - T1 - T2
           const float t1 = __uint_as_float(vr[jj]), t2 = __uint_as_float(vi[jj]);
-          const float a = (t1 - t2) * inv * inv2, b = (__uint_as_float(v3[jj]) - t1 - t2) * inv * inv2;
-          vmax = fmaxf(vmax, fmaxf(fabsf(a), fabsf(b)));
+          const float a = (t1 - t2) * sc * inv2, b = (__uint_as_float(v3[jj]) - t1 - t2) * sc * inv2;
+          if (!acc) vmax = fmaxf(vmax, fmaxf(fabsf(a), fabsf(b)));
           vr[jj] = __float_as_uint(a);
           vi[jj] = __float_as_uint(b);
         }
@@ -382,7 +411,7 @@ k_tc_gemm2(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorM
       }
       __syncwarp();
       auto ncols_of = [&](int rd) { const int64_t nl = p.N - (n0 + rd * 16); return nl < 16 ? (nl < 0 ? 0 : (int)nl) : 16; };
-      tg2_flush(p, ebuf, lane, q, mt, row, oc, O, n0, ncols_of(0), cn_s, staged);
+      tg2_flush(p, ebuf, lane, q, mt, row, oc, O, n0, ncols_of(0), cn_s, staged, acc, vmax);
       __syncwarp();
       // round 3 (still in registers) takes round 0's buffer
 #pragma unroll
@@ -391,13 +420,14 @@ k_tc_gemm2(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorM
                      "f"(__uint_as_float(vr[jj])), "f"(__uint_as_float(vi[jj])),
                      "f"(__uint_as_float(vr[jj + 1])), "f"(__uint_as_float(vi[jj + 1])) : "memory");
       __syncwarp();
-      tg2_flush(p, ebuf + TG2_EBUF, lane, q, mt, row, oc, O, n0 + 16, ncols_of(1), cn_s, staged);
-      tg2_flush(p, ebuf + 2 * TG2_EBUF, lane, q, mt, row, oc, O, n0 + 32, ncols_of(2), cn_s, staged);
-      tg2_flush(p, ebuf, lane, q, mt, row, oc, O, n0 + 48, ncols_of(3), cn_s, staged);
+      tg2_flush(p, ebuf + TG2_EBUF, lane, q, mt, row, oc, O, n0 + 16, ncols_of(1), cn_s, staged, acc, vmax);
+      tg2_flush(p, ebuf + 2 * TG2_EBUF, lane, q, mt, row, oc, O, n0 + 32, ncols_of(2), cn_s, staged, acc, vmax);
+      tg2_flush(p, ebuf, lane, q, mt, row, oc, O, n0 + 48, ncols_of(3), cn_s, staged, acc, vmax);
       __syncwarp();
-      if (p.amax_out) {                          // rows past M / padded columns hold zeros
+      if (p.amax_out && last) {                  // rows past M / padded columns hold zeros
         for (int o = 16; o; o >>= 1) vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
         if (lane == 0 && vmax > 0.f) atomicMax(reinterpret_cast<unsigned int*>(p.amax_out) + z, __float_as_uint(vmax));
+      }
       }
     }
   } else if (warp == MMA_WARP) {
@@ -409,10 +439,14 @@ k_tc_gemm2(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorM
       uint32_t bph = 0, aph = 0, tph = 0;
       const uint64_t dB = umma_desc(smem_u32(bring), 128, 256);
       constexpr uint32_t bstage16 = TG2_BSTAGE >> 4, bblk16 = TG2_BBLK >> 4;
-      for (int it = 0; it < nitems; ++it, tph ^= 1) {
-        mbar_wait_spin_cluster(tempty, tph ^ 1);
-        tc_fence_after();
+      const int kseg = p.kseg;
+      int cseg = 0;                                // chunks issued into the current K segment
+      for (int it = 0; it < nitems; ++it) {
         for (int c = 0; c < nchunk; ++c) {
+          if (cseg == 0) {                         // segment start: the epilogue has drained the accumulators
+            mbar_wait_spin_cluster(tempty, tph ^ 1);
+            tc_fence_after();
+          }
           mbar_wait_spin_cluster(&afull[stage], aph);
           mbar_wait_spin_cluster(&bfull[bs], bph);
           tc_fence_after();
@@ -422,7 +456,7 @@ k_tc_gemm2(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorM
             const uint32_t aih = arh + 8, ash = arh + 16, arl = arh + 24, ail = arh + 32, asl = arh + 40;
             const uint64_t brh = bb, bih = bb + bblk16, bsh = bb + 2 * bblk16;
             const uint64_t brl = bb + 3 * bblk16, bil = bb + 4 * bblk16, bsl = bb + 5 * bblk16;
-            const uint32_t first = c == 0 ? 0u : 1u;
+            const uint32_t first = cseg == 0 ? 0u : 1u;
             const uint32_t d1 = 0u, d2 = (uint32_t)NT, d3 = 2u * (uint32_t)NT;
             // small terms first (lo*hi, hi*lo), then hi*hi
             mma_f16_ts_pair(d1, arl, brh, idesc, first);
@@ -436,9 +470,10 @@ k_tc_gemm2(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorM
             mma_f16_ts_pair(d3, ash, bsh, idesc, 1u);
             umma_commit_pair(&aempty[stage]);
             umma_commit_pair(&bempty[bs]);
-            if (c == nchunk - 1) umma_commit_pair(tfull);
+            if (cseg + 1 == kseg || c == nchunk - 1) umma_commit_pair(tfull);
           }
           __syncwarp();
+          if (++cseg == kseg || c == nchunk - 1) { cseg = 0; tph ^= 1; }
           if (++bs == BS) { bs = 0; bph ^= 1; }
           if (++stage == AS) { stage = 0; aph ^= 1; }
         }

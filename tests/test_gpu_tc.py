@@ -265,6 +265,52 @@ def test_tc_gemm_f16_split_step(M, K, N, scale, sscale):
     assert torch.equal(amax_out, want), (amax_out, want)
 
 
+@pytest.mark.parametrize("M,K,N", [(8192, 8192, 128), (4096, 5120, 256), (2048, 16384, 128)])
+def test_tc_gemm_long_k_segments(M, K, N):
+    """K > 2048 on the CTA-pair kernel: the K loop leaves the tensor core every
+    2048 complex (fp32 round-to-nearest adds of the segment sums), so the
+    round-toward-zero accumulation inside the tensor core does not grow with K
+    (unsegmented: 1.5e-5 at K = 8192, 2.9e-5 at 16384); ragged last segment;
+    amax_out tracks the final sums."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2011_02621_b200 import _native as NV
+    from paper_2011_02621_b200.engine import ContractionPlan, NetworkSpec, PathExecutor
+
+    edges = {(0, 1): K, (0, 2): M, (1, 2): N}
+    legs = {0: [(0, 2), (0, 1)], 1: [(0, 1), (1, 2)], 2: [(0, 2), (1, 2)]}
+    spec = NetworkSpec([0, 1, 2], edges, legs)
+    g = torch.Generator(device="cuda")
+    g.manual_seed(M + K + N)
+    sites = {q: torch.randn((1,) + spec.site_dims(q), dtype=torch.complex64, device="cuda", generator=g) for q in range(3)}
+    plan = ContractionPlan(spec, [0, 1, 2])
+    ex = PathExecutor(plan, sites, dtype="complex64")
+    d = ex._steps[0]
+    Z = 2
+    acc = torch.randn(Z * M * K, dtype=torch.complex64, device="cuda", generator=g)
+    out = torch.zeros(Z * M * N, dtype=torch.complex64, device="cuda")
+    amax_in = torch.view_as_real(acc.reshape(Z, -1)).abs().reshape(Z, -1).amax(dim=1).contiguous()
+    amax_out = torch.zeros(Z, dtype=torch.float32, device="cuda")
+    d.Z, d.slices_per_b, d.s0 = Z, 1, 0
+    d.acc, d.acc_zstride = acc.data_ptr(), M * K
+    d.out, d.out_zstride = out.data_ptr(), M * N
+    d.site.sel = None
+    d.amax_in, d.amax_out = amax_in.data_ptr(), amax_out.data_ptr()
+    NV.check(NV.lib().tnc_step(C.byref(d), C.c_void_p(torch.cuda.current_stream().cuda_stream)), "tnc_step")
+    torch.cuda.synchronize()
+    site = ex.step_sites[0][0][0].reshape(K, N).to(torch.complex128)
+    ref = acc.reshape(Z, M, K).to(torch.complex128) @ site
+    got = out.reshape(Z, M, N).to(torch.complex128)
+    err = ((got - ref).norm() / ref.norm()).item()
+    assert err <= 6e-6, err
+    shrink = (torch.sum(got * ref.conj()).real / torch.sum(ref * ref.conj()).real).item() - 1.0
+    assert abs(shrink) <= 5e-7, shrink
+    want = torch.view_as_real(out.reshape(Z, -1)).abs().reshape(Z, -1).amax(dim=1)
+    assert torch.equal(amax_out, want), (amax_out, want)
+
+
 @pytest.mark.parametrize("dtype", ["complex64", "complex128"])
 @pytest.mark.parametrize("M,K,N", [(65536, 16, 1), (65536, 8, 4), (65536, 2, 2), (65536, 64, 3), (131072, 32, 2), (65536, 8, 16), (65536, 4, 8), (65536, 2, 16), (65536, 16, 12),
                                    (4, 16, 2048), (32, 2048, 16), (1, 512, 2), (1, 8192, 16), (256, 8192, 16),

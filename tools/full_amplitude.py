@@ -1,8 +1,10 @@
-"""Whole sliced amplitudes of a square-lattice circuit on the GPU, checked
-against the dense state vector (oracle) when the lattice has <= 24 qubits.
+"""Whole sliced amplitudes of a square-lattice or 53-qubit Sycamore circuit on
+the GPU, checked against the dense state vector (oracle) when the lattice has
+<= 24 qubits.
 
     python tools/full_amplitude.py --rows 5 --cols 4 --depth 16 --split 8 --cuts 4-8,11-15 \
         [--nbits 1] [--chunk 512] [--dtype complex64] [--json out.json]
+    python tools/full_amplitude.py --net syc53 --depth 12 --split 6 --cap 12 --cuts 9-14,2-8 --chunk 16
 
 All slices of the cut plan are contracted in chunks of ``--chunk`` slices
 (accumulated on the device); the JSON is rewritten after every chunk, so an
@@ -27,10 +29,11 @@ def main():
     import torch
 
     import tn_oracle as O  # checker only
-    from paper_2011_02621_b200 import generate_lattice, pattern_rqc, square_patterns
+    from paper_2011_02621_b200 import generate_lattice, pattern_rqc, square_patterns, sycamore53_graph
     from paper_2011_02621_b200.network import TwoSidedEngine
 
     ap = argparse.ArgumentParser()
+    ap.add_argument("--net", default="square", choices=["square", "syc53"])
     ap.add_argument("--rows", type=int, default=5)
     ap.add_argument("--cols", type=int, default=4)
     ap.add_argument("--depth", type=int, default=16)
@@ -41,18 +44,25 @@ def main():
     ap.add_argument("--chunk", type=int, default=512)
     ap.add_argument("--dtype", default="complex64")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--z", type=int, default=0, help="batch elements (bitstring x slice) per device pass (0: auto)")
     ap.add_argument("--json", default=None)
     ap.add_argument("--slice-lo", type=int, default=0, help="first slice of this run (a run cut off by a time "
                     "limit is continued from its JSON's slices_done; the partial sums add)")
     ap.add_argument("--slice-hi", type=int, default=-1)
     args = ap.parse_args()
     dev = torch.device("cuda", 0)
-    n = args.rows * args.cols
-    graph = generate_lattice("square", args.rows, args.cols)
-    circ = pattern_rqc(graph, square_patterns(args.rows, args.cols), args.depth, seed=args.seed)
+    if args.net == "syc53":
+        graph, pats, _ = sycamore53_graph()
+        circ = pattern_rqc(graph, [pats[c] for c in "ABCDCDAB"], args.depth, seed=args.seed)
+        n = 53
+    else:
+        n = args.rows * args.cols
+        graph = generate_lattice("square", args.rows, args.cols)
+        circ = pattern_rqc(graph, square_patterns(args.rows, args.cols), args.depth, seed=args.seed)
     cuts = [tuple(int(x) for x in c.split("-")) for c in args.cuts.split(",")] if args.cuts else None
     t0 = time.perf_counter()
-    eng = TwoSidedEngine(circ, split_cycle=args.split, cuts=cuts, max_rank=args.cap, dtype=args.dtype, device=dev)
+    eng = TwoSidedEngine(circ, split_cycle=args.split, cuts=cuts, max_rank=args.cap, dtype=args.dtype, device=dev,
+                         max_batch_elems=args.z or None)
     rng = np.random.default_rng(1000 + args.depth)
     outs = ["".join(rng.choice(["0", "1"], n)) for _ in range(args.nbits)]
     ex = eng.prepare(outs)
