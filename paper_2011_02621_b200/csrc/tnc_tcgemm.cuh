@@ -856,7 +856,15 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
     // stages: fill the shared-memory budget
     int RS = 4, BS = 3;
     const size_t budget = 226 * 1024;
-    p.cn_smem = (!d.c_rows_contig && d.N <= 1024 && d.out_zstride < 0x7fffffffLL) ? 1 : 0;
+    // the staged column offsets are int32: they fit when the result of one z does,
+    // or when the new legs' own extents and strides say so (2^32+-element results)
+    bool cn_fits = d.out_zstride < 0x7fffffffLL;
+    if (!cn_fits && d.nn > 0) {
+      int64_t mx = 0;
+      for (int j = 0; j < d.nn; ++j) mx += (d.n_dim[j] - 1) * d.n_cstride[j];
+      cn_fits = mx < 0x7fffffffLL;
+    }
+    p.cn_smem = (!d.c_rows_contig && d.N <= 1024 && cn_fits) ? 1 : 0;
     // contiguous 32 x 16 blocks: innermost free leg (>= 32 rows) at stride 16 and
     // 16 consecutive columns contiguous (innermost new leg of extent % 16 == 0 at stride 1)
     p.blk_contig = 0;
@@ -886,7 +894,7 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
     const bool pair = tg2_applicable(p);
     if (pair) {
       // pair kernel: 96 KB result stage, 12 KB B' half stages
-      p.cn_smem = (!d.c_rows_contig && d.N <= 2048 && d.out_zstride < 0x7fffffffLL) ? 1 : 0;
+      p.cn_smem = (!d.c_rows_contig && d.N <= 2048 && cn_fits) ? 1 : 0;
       const int64_t cn2 = p.cn_smem ? d.N : 0;
       RS = 3; BS = 3;
       while (RS + 1 <= TG2_MAX_RS && RS < 5 && tg2_smem_bytes(RS + 1, BS, cn2) <= budget) ++RS;
