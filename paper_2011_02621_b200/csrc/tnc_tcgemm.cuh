@@ -510,11 +510,12 @@ k_tc_gemm(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMa
       const int64_t row = mt * 128 + r;
       int64_t oc = row * p.N;
       if (!p.c_rows_contig && row < p.M) {
-        int64_t f = row;
+        uint32_t f = (uint32_t)row;              // M < 2^31 (try_tc_gemm): 32-bit divisions
         oc = 0;
         for (int jj = p.nf - 1; jj >= 0; --jj) {
-          const int64_t qq = f / p.f_dim[jj];
-          oc += (f - qq * p.f_dim[jj]) * p.f_cstride[jj];
+          const uint32_t dd = (uint32_t)p.f_dim[jj];
+          const uint32_t qq = f / dd;
+          oc += (int64_t)(f - qq * dd) * p.f_cstride[jj];
           f = qq;
         }
       }
@@ -962,7 +963,8 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
       static uint64_t attr2 = 0;
       int adev2 = 0;
       if (attr_needed(attr2, &adev2)) {
-        cudaFuncSetAttribute(k_tc_gemm2, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_tc_gemm2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_tc_gemm2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr2 |= 1ull << (adev2 & 63);
       }
       const int64_t W = p.Z * ((p.tiles_m + 1) / 2) * p.tiles_n;
@@ -982,11 +984,12 @@ int try_tc_gemm(const tnc_step_desc& d, cudaStream_t s) {
         lc.attrs = &la;
         lc.numAttrs = 1;
         int nc = 0;
-        if (cudaOccupancyMaxActiveClusters(&nc, k_tc_gemm2, &lc) == cudaSuccess && nc > 0) max_pairs = std::min(max_pairs, nc);
+        if (cudaOccupancyMaxActiveClusters(&nc, k_tc_gemm2<true>, &lc) == cudaSuccess && nc > 0) max_pairs = std::min(max_pairs, nc);
         else cudaGetLastError();
       }
       const int64_t npairs = std::min<int64_t>(max_pairs, W);
-      k_tc_gemm2<<<(unsigned)(2 * npairs), TG2_THREADS, smem2, s>>>(p, tm, tmb);
+      if (p.nchunk > p.kseg) k_tc_gemm2<true><<<(unsigned)(2 * npairs), TG2_THREADS, smem2, s>>>(p, tm, tmb);
+      else k_tc_gemm2<false><<<(unsigned)(2 * npairs), TG2_THREADS, smem2, s>>>(p, tm, tmb);
     } else if (p.g3) k_tc_gemm<16, true, true><<<(unsigned)grid, TG_THREADS_G3, smem, s>>>(p, tm);
     else if (f16) k_tc_gemm<16, true><<<(unsigned)grid, TG_THREADS_G3, smem, s>>>(p, tm);
     else if (KC == 16) k_tc_gemm<16, false><<<(unsigned)grid, TG_THREADS, smem, s>>>(p, tm);

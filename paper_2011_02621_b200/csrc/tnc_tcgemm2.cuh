@@ -139,16 +139,18 @@ __device__ __forceinline__ uint32_t tg2_piece(uint32_t buf_s, int row, int piece
 // `acc`: a later K segment of the tile -- the partial product is added to the
 // stored one in fp32 round-to-nearest (the same thread stored it);
 // `vmax`: max |re|, |im| of the final values (tracked on the last segment)
+template <bool SEG>
 __device__ __forceinline__ void tg2_st4(float4* dst, float4 v, bool acc, float& vmax) {
-  if (acc) {
+  if (SEG && acc) {
     const float4 o = *dst;
     v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
     vmax = fmaxf(vmax, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
   }
   __stcs(dst, v);
 }
+template <bool SEG>
 __device__ __forceinline__ void tg2_st2(float2* dst, float2 v, bool acc, float& vmax) {
-  if (acc) {
+  if (SEG && acc) {
     const float2 o = *dst;
     v.x += o.x; v.y += o.y;
     vmax = fmaxf(vmax, fmaxf(fabsf(v.x), fabsf(v.y)));
@@ -158,6 +160,7 @@ __device__ __forceinline__ void tg2_st2(float2* dst, float2 v, bool acc, float& 
 
 // the warp's 32 rows x 16 columns [n0c0, n0c0 + ncols) of the result, from a
 // staged round buffer to global memory (layouts as k_tc_gemm's epilogue)
+template <bool SEG>
 __device__ __forceinline__ void tg2_flush(const GemmDesc& p, uint32_t buf_s, int lane, int q, int64_t mt, int64_t row,
                                           int64_t oc, float2* O, int64_t n0c0, int ncols, const int32_t* cn_s,
                                           bool staged, bool acc, float& vmax) {
@@ -171,7 +174,7 @@ __device__ __forceinline__ void tg2_flush(const GemmDesc& p, uint32_t buf_s, int
         float4 v;
         asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                      : "r"(tg2_piece(buf_s, c >> 3, c & 7)) : "memory");
-        tg2_st4(dst + c, v, acc, vmax);
+        tg2_st4<SEG>(dst + c, v, acc, vmax);
       }
       return;
     }
@@ -192,10 +195,10 @@ __device__ __forceinline__ void tg2_flush(const GemmDesc& p, uint32_t buf_s, int
                      : "r"(tg2_piece(buf_s, lr, sub)) : "memory");
         float2* dst = O + ocr + a0;
         if (2 * sub + 1 < ncols && a1 == a0 + 1 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-          tg2_st4(reinterpret_cast<float4*>(dst), v, acc, vmax);
+          tg2_st4<SEG>(reinterpret_cast<float4*>(dst), v, acc, vmax);
         } else {
-          tg2_st2(dst, make_float2(v.x, v.y), acc, vmax);
-          if (2 * sub + 1 < ncols) tg2_st2(O + ocr + a1, make_float2(v.z, v.w), acc, vmax);
+          tg2_st2<SEG>(dst, make_float2(v.x, v.y), acc, vmax);
+          if (2 * sub + 1 < ncols) tg2_st2<SEG>(O + ocr + a1, make_float2(v.z, v.w), acc, vmax);
         }
       }
     }
@@ -210,16 +213,19 @@ __device__ __forceinline__ void tg2_flush(const GemmDesc& p, uint32_t buf_s, int
                    : "r"(tg2_piece(buf_s, lane, u)) : "memory");
       if (2 * u < ncols) {
         const int64_t n = n0c0 + 2 * u;
-        tg2_st2(O + oc + (p.cn_smem ? (int64_t)cn_s[n] : p.c_noff[n]), make_float2(v.x, v.y), acc, vmax);
+        tg2_st2<SEG>(O + oc + (p.cn_smem ? (int64_t)cn_s[n] : p.c_noff[n]), make_float2(v.x, v.y), acc, vmax);
       }
       if (2 * u + 1 < ncols) {
         const int64_t n = n0c0 + 2 * u + 1;
-        tg2_st2(O + oc + (p.cn_smem ? (int64_t)cn_s[n] : p.c_noff[n]), make_float2(v.z, v.w), acc, vmax);
+        tg2_st2<SEG>(O + oc + (p.cn_smem ? (int64_t)cn_s[n] : p.c_noff[n]), make_float2(v.z, v.w), acc, vmax);
       }
     }
   }
 }
 
+// SEG: K longer than one segment (the accumulate paths of the epilogue are
+// compiled only then: they cost registers in the drain, 3.7% on the K <= 2048 steps)
+template <bool SEG>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TG2_THREADS, 1)
 k_tc_gemm2(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorMap tmA,
            const __grid_constant__ CUtensorMap tmB) {
@@ -346,18 +352,19 @@ k_tc_gemm2(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorM
     float inv = 1.f, inv2 = 1.f;
     int64_t inv_z = -1;
     uint32_t tph = 0;
-    const int kseg = p.kseg;                     // chunks accumulated in TMEM before the sum leaves the tensor core
+    const int kseg = SEG ? p.kseg : nchunk;      // chunks accumulated in TMEM before the sum leaves the tensor core
     for (int it = 0; it < nitems; ++it) {
       int64_t z, mt, nt;
       item(it, z, mt, nt);
       const int64_t row = mt * 128 + r;
       int64_t oc = row * p.N;
       if (!p.c_rows_contig && row < p.M) {
-        int64_t f = row;
+        uint32_t f = (uint32_t)row;              // M < 2^31 (try_tc_gemm): 32-bit divisions
         oc = 0;
         for (int jj = p.nf - 1; jj >= 0; --jj) {
-          const int64_t qq = f / p.f_dim[jj];
-          oc += (f - qq * p.f_dim[jj]) * p.f_cstride[jj];
+          const uint32_t dd = (uint32_t)p.f_dim[jj];
+          const uint32_t qq = f / dd;
+          oc += (int64_t)(f - qq * dd) * p.f_cstride[jj];
           f = qq;
         }
       }
@@ -374,7 +381,7 @@ k_tc_gemm2(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorM
       // round-toward-zero chain inside the tensor core stays short
       for (int c0 = 0; c0 < nchunk; c0 += kseg, tph ^= 1) {
       const int c1 = min(nchunk, c0 + kseg);
-      const bool acc = c0 > 0, last = c1 == nchunk;
+      const bool acc = SEG && c0 > 0, last = !SEG || c1 == nchunk;
       const float sc = inv * (1.f + TG_RZ_LOSS * (float)(3 * (c1 - c0)));
       float vmax = 0.f;
       mbar_wait_idle(tfull, tph);
@@ -397,7 +404,7 @@ k_tc_gemm2(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorM
         for (int jj = 0; jj < 16; ++jj) {          // re = T1 - T2, im = T3 - T1 - T2
           const float t1 = __uint_as_float(vr[jj]), t2 = __uint_as_float(vi[jj]);
           const float a = (t1 - t2) * sc * inv2, b = (__uint_as_float(v3[jj]) - t1 - t2) * sc * inv2;
-          if (!acc) vmax = fmaxf(vmax, fmaxf(fabsf(a), fabsf(b)));
+          if (!SEG || !acc) vmax = fmaxf(vmax, fmaxf(fabsf(a), fabsf(b)));
           vr[jj] = __float_as_uint(a);
           vi[jj] = __float_as_uint(b);
         }
@@ -411,7 +418,7 @@ k_tc_gemm2(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorM
       }
       __syncwarp();
       auto ncols_of = [&](int rd) { const int64_t nl = p.N - (n0 + rd * 16); return nl < 16 ? (nl < 0 ? 0 : (int)nl) : 16; };
-      tg2_flush(p, ebuf, lane, q, mt, row, oc, O, n0, ncols_of(0), cn_s, staged, acc, vmax);
+      tg2_flush<SEG>(p, ebuf, lane, q, mt, row, oc, O, n0, ncols_of(0), cn_s, staged, acc, vmax);
       __syncwarp();
       // round 3 (still in registers) takes round 0's buffer
 #pragma unroll
@@ -420,9 +427,9 @@ k_tc_gemm2(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorM
                      "f"(__uint_as_float(vr[jj])), "f"(__uint_as_float(vi[jj])),
                      "f"(__uint_as_float(vr[jj + 1])), "f"(__uint_as_float(vi[jj + 1])) : "memory");
       __syncwarp();
-      tg2_flush(p, ebuf + TG2_EBUF, lane, q, mt, row, oc, O, n0 + 16, ncols_of(1), cn_s, staged, acc, vmax);
-      tg2_flush(p, ebuf + 2 * TG2_EBUF, lane, q, mt, row, oc, O, n0 + 32, ncols_of(2), cn_s, staged, acc, vmax);
-      tg2_flush(p, ebuf, lane, q, mt, row, oc, O, n0 + 48, ncols_of(3), cn_s, staged, acc, vmax);
+      tg2_flush<SEG>(p, ebuf + TG2_EBUF, lane, q, mt, row, oc, O, n0 + 16, ncols_of(1), cn_s, staged, acc, vmax);
+      tg2_flush<SEG>(p, ebuf + 2 * TG2_EBUF, lane, q, mt, row, oc, O, n0 + 32, ncols_of(2), cn_s, staged, acc, vmax);
+      tg2_flush<SEG>(p, ebuf, lane, q, mt, row, oc, O, n0 + 48, ncols_of(3), cn_s, staged, acc, vmax);
       __syncwarp();
       if (p.amax_out && last) {                  // rows past M / padded columns hold zeros
         for (int o = 16; o; o >>= 1) vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
@@ -439,7 +446,7 @@ k_tc_gemm2(const __grid_constant__ GemmDesc p, const __grid_constant__ CUtensorM
       uint32_t bph = 0, aph = 0, tph = 0;
       const uint64_t dB = umma_desc(smem_u32(bring), 128, 256);
       constexpr uint32_t bstage16 = TG2_BSTAGE >> 4, bblk16 = TG2_BBLK >> 4;
-      const int kseg = p.kseg;
+      const int kseg = SEG ? p.kseg : nchunk;
       int cseg = 0;                                // chunks issued into the current K segment
       for (int it = 0; it < nitems; ++it) {
         for (int c = 0; c < nchunk; ++c) {
