@@ -22,8 +22,13 @@ __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
 // grid: (tiles_m * tiles_n) per z, z-major
 __global__ void __launch_bounds__(DM_THREADS)
 k_dmma_c128(const __grid_constant__ tnc_step_desc d, int64_t tiles_m, int64_t tiles_n) {
-  __shared__ __align__(16) double As[DM_BM][DM_BK + 4];   // [row][k'] (padded: 2-wavefront reads)
-  __shared__ __align__(16) double Bs[DM_BK][DM_BN + 4];   // [k'][n']
+  // two smem stages; the next stage's global loads are issued into registers
+  // before the current stage's DMMAs and stored after them (the synchronous
+  // load -> sync -> DMMA loop left the DMMA sub-pipe 57% active, ncu)
+  extern __shared__ __align__(16) unsigned char dm_smem[];
+  double (*As)[DM_BM][DM_BK + 4] = reinterpret_cast<double (*)[DM_BM][DM_BK + 4]>(dm_smem);   // [stage][row][k'] (padded)
+  double (*Bs)[DM_BK][DM_BN + 4] =
+      reinterpret_cast<double (*)[DM_BK][DM_BN + 4]>(dm_smem + 2 * sizeof(double) * DM_BM * (DM_BK + 4));  // [stage][k'][n']
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int64_t t = blockIdx.x;
   const int64_t tiles = tiles_m * tiles_n;
@@ -34,48 +39,83 @@ k_dmma_c128(const __grid_constant__ tnc_step_desc d, int64_t tiles_m, int64_t ti
   const double2* A = reinterpret_cast<const double2*>(d.acc) + z * d.acc_zstride;
   const double2* S = reinterpret_cast<const double2*>(d.site.ptr) + site_offset(d.site, z, d.slices_per_b, d.s0);
   double2* O = reinterpret_cast<double2*>(d.out) + z * d.out_zstride;
-  const int Kr = (int)(2 * d.K), Nr = (int)(2 * d.N);
+  const int Kr = (int)(2 * d.K);
   double acc[2][8][2];
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  for (int k0 = 0; k0 < Kr; k0 += DM_BK) {
-    // A stage: 64 rows x 16 complex (rows contiguous: row r at r*K complex)
-    for (int e = threadIdx.x; e < DM_BM * (DM_BK / 2); e += DM_THREADS) {
+  constexpr int NA = DM_BM * (DM_BK / 2) / DM_THREADS;          // 8 A elements per thread and stage
+  constexpr int NB = (DM_BK / 2) * (DM_BN / 2) / DM_THREADS;    // 4 site elements
+  double2 ra[NA], rb[NB];
+  // this thread's site columns do not change over the K loop
+  int64_t bno[NB];
+  bool bnv[NB];
+#pragma unroll
+  for (int u = 0; u < NB; ++u) {
+    const int e = threadIdx.x + u * DM_THREADS;
+    const int64_t n = n0r / 2 + e % (DM_BN / 2);
+    bnv[u] = n < d.N;
+    bno[u] = bnv[u] ? d.b_noff[n] : 0;
+  }
+  auto fetch = [&](int k0) {
+#pragma unroll
+    for (int u = 0; u < NA; ++u) {
+      const int e = threadIdx.x + u * DM_THREADS;
       const int r = e / (DM_BK / 2), kc = e % (DM_BK / 2);
       const int64_t row = m0 + r, k = k0 / 2 + kc;
-      double2 v = make_double2(0.0, 0.0);
-      if (row < d.M && k < d.K) v = A[row * d.K + k];
-      As[r][2 * kc] = v.x;
-      As[r][2 * kc + 1] = v.y;
+      ra[u] = (row < d.M && k < d.K) ? A[row * d.K + k] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < NB; ++u) {
+      const int e = threadIdx.x + u * DM_THREADS;
+      const int64_t k = k0 / 2 + e / (DM_BN / 2);
+      double2 sv = make_double2(0.0, 0.0);
+      if (k < d.K && bnv[u]) {
+        sv = S[d.b_koff[k] + bno[u]];
+        if (d.conj_b) sv.y = -sv.y;
+      }
+      rb[u] = sv;
+    }
+  };
+  auto stash = [&](int st) {
+#pragma unroll
+    for (int u = 0; u < NA; ++u) {
+      const int e = threadIdx.x + u * DM_THREADS;
+      const int r = e / (DM_BK / 2), kc = e % (DM_BK / 2);
+      As[st][r][2 * kc] = ra[u].x;
+      As[st][r][2 * kc + 1] = ra[u].y;
     }
     // B' stage: rows k' = 2k + c, cols n' = 2n + c'
-    for (int e = threadIdx.x; e < (DM_BK / 2) * (DM_BN / 2); e += DM_THREADS) {
+#pragma unroll
+    for (int u = 0; u < NB; ++u) {
+      const int e = threadIdx.x + u * DM_THREADS;
       const int kc = e / (DM_BN / 2), nc = e % (DM_BN / 2);
-      const int64_t k = k0 / 2 + kc, n = n0r / 2 + nc;
-      double2 s = make_double2(0.0, 0.0);
-      if (k < d.K && n < d.N) {
-        s = S[d.b_koff[k] + d.b_noff[n]];
-        if (d.conj_b) s.y = -s.y;
-      }
-      Bs[2 * kc][2 * nc] = s.x;      Bs[2 * kc][2 * nc + 1] = s.y;
-      Bs[2 * kc + 1][2 * nc] = -s.y; Bs[2 * kc + 1][2 * nc + 1] = s.x;
+      Bs[st][2 * kc][2 * nc] = rb[u].x;      Bs[st][2 * kc][2 * nc + 1] = rb[u].y;
+      Bs[st][2 * kc + 1][2 * nc] = -rb[u].y; Bs[st][2 * kc + 1][2 * nc + 1] = rb[u].x;
     }
-    __syncthreads();
+  };
+  fetch(0);
+  stash(0);
+  __syncthreads();
+  int st = 0;
+  for (int k0 = 0; k0 < Kr; k0 += DM_BK, st ^= 1) {
+    const bool more = k0 + DM_BK < Kr;
+    if (more) fetch(k0 + DM_BK);                   // in flight during this stage's DMMAs
 #pragma unroll
     for (int ks = 0; ks < DM_BK; ks += 4) {
       double af[2], bf[8];
 #pragma unroll
-      for (int i = 0; i < 2; ++i) af[i] = As[warp * 16 + i * 8 + (lane >> 2)][ks + (lane & 3)];
+      for (int i = 0; i < 2; ++i) af[i] = As[st][warp * 16 + i * 8 + (lane >> 2)][ks + (lane & 3)];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) bf[j] = Bs[ks + (lane & 3)][j * 8 + (lane >> 2)];
+      for (int j = 0; j < 8; ++j) bf[j] = Bs[st][ks + (lane & 3)][j * 8 + (lane >> 2)];
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
         for (int j = 0; j < 8; ++j) dmma_8x8x4(acc[i][j], af[i], bf[j]);
     }
+    if (more) stash(st ^ 1);                       // the other stage: last read before the previous barrier
     __syncthreads();
   }
   // C fragment: row = lane/4, real cols 2*(lane%4), +1  -> one complex per fragment
@@ -105,7 +145,14 @@ int try_dmma(const tnc_step_desc& d, cudaStream_t s) {
     const int64_t tm = (d.M + DM_BM - 1) / DM_BM, tn = (2 * d.N + DM_BN - 1) / DM_BN;
     const int64_t blocks = d.Z * tm * tn;
     if (blocks <= 0 || blocks > 0x7fffffffLL) return 0;
-    k_dmma_c128<<<(unsigned)blocks, DM_THREADS, 0, s>>>(d, tm, tn);
+    constexpr size_t smem = 2 * sizeof(double) * (DM_BM * (DM_BK + 4) + DM_BK * (DM_BN + 4));   // 70 KB: two stages
+    static uint64_t attr = 0;
+    int adev = 0;
+    if (attr_needed(attr, &adev)) {
+      cudaFuncSetAttribute(k_dmma_c128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr |= 1ull << (adev & 63);
+    }
+    k_dmma_c128<<<(unsigned)blocks, DM_THREADS, smem, s>>>(d, tm, tn);
     return cudaGetLastError() == cudaSuccess ? 1 : -1;
   }
 }
